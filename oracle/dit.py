@@ -1,0 +1,141 @@
+"""TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+CPU restatement of the DiT-shaped noise predictor pinned in
+``paper_2505_14741_b200/spec.py``, written directly from that docstring in
+plain numpy (float64 by default). It is independent of the CUDA code: the
+only thing shared is the table of dimensions.
+
+No reference implementation exists for this network (the reference predictor
+is an MLP, pkg/src/parastep/predictor.py:133-150), so its *arithmetic* is
+parity-unpinned; its API contract ``pred(x, t, T) -> eps`` is the one the
+reference sampler consumes (engines.py:40), which is how the golden fixtures
+drive it through the reference's own engines.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from paper_2505_14741_b200.spec import DiTSpec, layer_table
+
+from .core import P_WEIGHT, make_stream, time_embed, uniforms
+
+
+def _sincos_1d(d: int, pos: np.ndarray) -> np.ndarray:
+    half = d // 2
+    w = 10000.0 ** (-np.arange(half, dtype=np.float64) / half)
+    ang = pos[:, None].astype(np.float64) * w[None, :]
+    return np.concatenate([np.sin(ang), np.cos(ang)], axis=1)
+
+
+def pos_table(s: DiTSpec) -> np.ndarray:
+    f, h, w = np.meshgrid(np.arange(s.frames), np.arange(s.grid_h), np.arange(s.grid_w),
+                          indexing="ij")
+    f, h, w = f.ravel(), h.ravel(), w.ravel()
+    D = s.hidden
+    if s.frames == 1:
+        return np.concatenate([_sincos_1d(D // 2, h), _sincos_1d(D // 2, w)], axis=1)
+    return np.concatenate(
+        [_sincos_1d(D // 4, f), _sincos_1d(3 * D // 8, h), _sincos_1d(3 * D // 8, w)], axis=1)
+
+
+def init_params(s: DiTSpec, seed: int, bias_scale: float = 0.0) -> dict[str, tuple]:
+    """Xavier-uniform per the reference convention; optional nonzero test biases.
+
+    Test biases (not part of the reference convention; they only exercise the
+    bias path) draw from stream (6<<32)|i: b = (2u-1)*bias_scale.
+    """
+    out = {}
+    for i, (name, fi, fo) in enumerate(layer_table(s)):
+        lim = math.sqrt(6.0 / (fi + fo))
+        u = uniforms(seed, make_stream(P_WEIGHT, i), fi * fo)
+        W = ((2.0 * u - 1.0) * lim).reshape(fi, fo)
+        if bias_scale:
+            ub = uniforms(seed, make_stream(6, i), fo)
+            b = (2.0 * ub - 1.0) * bias_scale
+        else:
+            b = np.zeros(fo)
+        out[name] = (W, b)
+    return out
+
+
+def _latent_to_tokens(s: DiTSpec, x: np.ndarray) -> np.ndarray:
+    p = s.patch
+    if s.layout == "CHW":
+        v = x.reshape(s.channels, s.frames, s.height, s.width)
+    else:
+        v = x.reshape(s.frames, s.height, s.width, s.channels).transpose(3, 0, 1, 2)
+    # v: C, F, H, W -> tokens (f, hp, wp), features (c, ph, pw)
+    v = v.reshape(s.channels, s.frames, s.grid_h, p, s.grid_w, p)
+    v = v.transpose(1, 2, 4, 0, 3, 5)
+    return v.reshape(s.tokens, s.patch_dim)
+
+
+def _tokens_to_latent(s: DiTSpec, tok: np.ndarray) -> np.ndarray:
+    p = s.patch
+    v = tok.reshape(s.frames, s.grid_h, s.grid_w, s.channels, p, p)
+    v = v.transpose(3, 0, 1, 4, 2, 5).reshape(s.channels, s.frames, s.height, s.width)
+    if s.layout == "FHWC":
+        v = v.transpose(1, 2, 3, 0)
+    return v.reshape(-1)
+
+
+def _ln(x: np.ndarray) -> np.ndarray:
+    mu = x.mean(axis=-1, keepdims=True)
+    var = ((x - mu) ** 2).mean(axis=-1, keepdims=True)
+    return (x - mu) / np.sqrt(var + 1e-6)
+
+
+def _silu(x):
+    return x / (1.0 + np.exp(-x))
+
+
+def _gelu_tanh(x):
+    return 0.5 * x * (1.0 + np.tanh(math.sqrt(2.0 / math.pi) * (x + 0.044715 * (x * x * x))))
+
+
+class DiT:
+    """pred(x, t, T) -> eps for one latent vector."""
+
+    def __init__(self, s: DiTSpec, seed: int = 0, bias_scale: float = 0.0,
+                 dtype=np.float64):
+        s.validate()
+        self.s = s
+        self.dtype = dtype
+        self.params = {k: (W.astype(dtype), b.astype(dtype))
+                       for k, (W, b) in init_params(s, seed, bias_scale).items()}
+        self.pos = pos_table(s).astype(dtype)
+        self.data_dim = s.data_dim
+
+    def _lin(self, name, a):
+        W, b = self.params[name]
+        return a @ W + b
+
+    def __call__(self, x: np.ndarray, t: int, T: int) -> np.ndarray:
+        s, dt = self.s, self.dtype
+        D, H, dh = s.hidden, s.heads, s.head_dim
+        tok = _latent_to_tokens(s, np.asarray(x, dtype=np.float64)).astype(dt)
+        h = self._lin("patch", tok) + self.pos
+        c = self._lin("temb2", _silu(self._lin("temb1", time_embed(t, s.freq_dim).astype(dt))))
+        sc = _silu(c)
+        L = s.tokens
+        for i in range(s.depth):
+            m = self._lin(f"b{i}.ada", sc)
+            sh1, sc1, g1, sh2, sc2, g2 = (m[k * D:(k + 1) * D] for k in range(6))
+            a = _ln(h) * (1.0 + sc1) + sh1
+            qkv = self._lin(f"b{i}.qkv", a).reshape(L, 3, H, dh)
+            q, k, v = qkv[:, 0].transpose(1, 0, 2), qkv[:, 1].transpose(1, 0, 2), \
+                qkv[:, 2].transpose(1, 0, 2)
+            sco = (q @ k.transpose(0, 2, 1)) / math.sqrt(dh)
+            sco = np.exp(sco - sco.max(axis=-1, keepdims=True))
+            pr = sco / sco.sum(axis=-1, keepdims=True)
+            o = (pr @ v).transpose(1, 0, 2).reshape(L, D)
+            h = h + g1 * self._lin(f"b{i}.proj", o)
+            a = _ln(h) * (1.0 + sc2) + sh2
+            h = h + g2 * self._lin(f"b{i}.fc2", _gelu_tanh(self._lin(f"b{i}.fc1", a)))
+        m = self._lin("final.ada", sc)
+        shf, scf = m[:D], m[D:]
+        out = self._lin("final.out", _ln(h) * (1.0 + scf) + shf)
+        return _tokens_to_latent(s, out.astype(np.float64))

@@ -1,0 +1,133 @@
+"""Architecture tables for the DiT-shaped noise predictors (no compute here).
+
+The reference predictor is a 2-D toy MLP (pkg/src/parastep/predictor.py:133-150);
+BASELINE.json's configs name DiT-shaped predictors the reference never
+defines. This file pins them once, shared by the CUDA product path
+(``dit.py``) and the CPU oracle (``oracle/dit.py``), so both build the same
+network from the same seed:
+
+* conditioning is the timestep only (the reference omits the conditioning
+  signal c, R/SPEC.md:8); the frequency embedding uses the reference's own
+  ``time_embed`` convention (predictor.py:44-65) at width ``freq_dim``;
+* weights use the reference's Xavier-uniform init convention
+  (predictor.py:202-215): layer i draws fan_in*fan_out uniforms from stream
+  (WEIGHT_INIT<<32)|i, W = (2u-1)*sqrt(6/(fan_in+fan_out)) reshaped
+  (fan_in, fan_out) row-major, zero bias. ``layer_table`` fixes the order i.
+  (No adaLN-Zero: zero-init gates would make every block the identity.)
+
+Block (DiT, adaLN modulation from SiLU(c)):
+    mod = SiLU(c) @ W_ada + b_ada -> shift1, scale1, gate1, shift2, scale2, gate2
+    x += gate1 * (attn(LN(x) * (1 + scale1) + shift1) @ W_o + b_o)
+    x += gate2 * (gelu_tanh((LN(x) * (1 + scale2) + shift2) @ W_1 + b_1) @ W_2 + b_2)
+LN has no affine parameters, eps 1e-6. Final layer: adaLN shift/scale, LN,
+linear to patch*patch*C. Patch vectors are ordered (c, ph, pw); tokens are
+ordered (f, hp, wp) row-major.
+
+Fixed sin-cos position embedding added after the patch projection:
+    e1(d, pos)[k]       = sin(pos * w_k),  e1(d, pos)[d/2 + k] = cos(pos * w_k),
+    w_k = 10000^(-k/(d/2)),  k < d/2
+    F == 1:  [e1(D/2, hp), e1(D/2, wp)]
+    F  > 1:  [e1(D/4, f), e1(3D/8, hp), e1(3D/8, wp)]
+
+Latent layouts (the RNG counter is the flat index in this order, so the
+layout must equal the flatten order the reference's 1-D vector uses):
+    "CHW"  — C x H x W (F = 1), e.g. 4x32x32
+    "FHWC" — F x H x W x C, channels-last, e.g. 13x60x90x16
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+
+@dataclass(frozen=True)
+class DiTSpec:
+    name: str
+    channels: int
+    frames: int
+    height: int
+    width: int
+    layout: str  # "CHW" or "FHWC"
+    patch: int
+    hidden: int
+    depth: int
+    heads: int
+    mlp_ratio: int = 4
+    freq_dim: int = 256
+
+    @property
+    def data_dim(self) -> int:
+        return self.channels * self.frames * self.height * self.width
+
+    @property
+    def grid_h(self) -> int:
+        return self.height // self.patch
+
+    @property
+    def grid_w(self) -> int:
+        return self.width // self.patch
+
+    @property
+    def tokens(self) -> int:
+        return self.frames * self.grid_h * self.grid_w
+
+    @property
+    def patch_dim(self) -> int:
+        return self.channels * self.patch * self.patch
+
+    @property
+    def head_dim(self) -> int:
+        return self.hidden // self.heads
+
+    @property
+    def mlp_hidden(self) -> int:
+        return self.hidden * self.mlp_ratio
+
+    def validate(self) -> None:
+        if self.layout not in ("CHW", "FHWC"):
+            raise ValueError(f"unknown latent layout {self.layout!r}")
+        if self.layout == "CHW" and self.frames != 1:
+            raise ValueError("CHW layout has a single frame")
+        if self.height % self.patch or self.width % self.patch:
+            raise ValueError("latent size must be a multiple of the patch")
+        if self.hidden % self.heads:
+            raise ValueError("hidden must divide into heads")
+        if self.hidden % 4 or self.freq_dim % 2:
+            raise ValueError("hidden must be a multiple of 4, freq_dim even")
+
+    def flops_per_forward(self) -> int:
+        """2 x MACs of all GEMMs + attention (QK^T and PV), one sample."""
+        L, D = self.tokens, self.hidden
+        per_block = L * D * (3 * D + D + 2 * self.mlp_hidden)
+        gemm = L * self.patch_dim * D + self.depth * per_block + L * D * self.patch_dim
+        attn = self.depth * 2 * L * L * D
+        return 2 * (gemm + attn)
+
+
+def layer_table(s: DiTSpec) -> list[tuple[str, int, int]]:
+    """(name, fan_in, fan_out) in init-stream order."""
+    D = s.hidden
+    out = [("patch", s.patch_dim, D), ("temb1", s.freq_dim, D), ("temb2", D, D)]
+    for i in range(s.depth):
+        out += [
+            (f"b{i}.ada", D, 6 * D),
+            (f"b{i}.qkv", D, 3 * D),
+            (f"b{i}.proj", D, D),
+            (f"b{i}.fc1", D, s.mlp_hidden),
+            (f"b{i}.fc2", s.mlp_hidden, D),
+        ]
+    out += [("final.ada", D, 2 * D), ("final.out", D, s.patch_dim)]
+    return out
+
+
+SPECS = {
+    # test-sized
+    "dit_tiny": DiTSpec("dit_tiny", 4, 1, 8, 8, "CHW", 2, 64, 2, 2, freq_dim=32),
+    "dit_tiny_video": DiTSpec("dit_tiny_video", 4, 3, 8, 12, "FHWC", 2, 96, 2, 3, freq_dim=32),
+    # BASELINE.json configs[0..1]: "small random-init DiT", latent 4x32x32
+    "dit_s2": DiTSpec("dit_s2", 4, 1, 32, 32, "CHW", 2, 384, 12, 6),
+    # configs[2]: DiT-XL/2-shaped
+    "dit_xl2": DiTSpec("dit_xl2", 4, 1, 32, 32, "CHW", 2, 1152, 28, 16),
+    # configs[3]: CogVideoX-2b-shaped, latent 13x60x90x16 (channels-last)
+    "cogvideox_2b": DiTSpec("cogvideox_2b", 16, 13, 60, 90, "FHWC", 2, 1920, 30, 30),
+}

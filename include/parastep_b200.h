@@ -1,0 +1,157 @@
+/*
+ * parastep_b200 — C-ABI of the B200-native ParaStep hot path.
+ *
+ * The reference (pkg/src/parastep, pure Python/numpy) has no FFI; its
+ * drop-in boundary is the Python module API bound by name at import:
+ *   - predictor.forward / forward_batch      (engines.py:40, worker.py:45)
+ *   - schedule.ddpm_step                      (engines.py:41, worker.py:46)
+ *   - numerics.draw_normal / RngStream        (engines.py:172-179)
+ * Each entry point below replaces the arithmetic behind one of those
+ * functions; the Python package paper_2505_14741_b200 restores the
+ * reference's signatures and exceptions on top of it (ctypes binding in
+ * paper_2505_14741_b200/_lib.py; INTEGRATION.md shows the binding).
+ *
+ * Conventions: all pointers are DEVICE pointers unless named host_*; every
+ * call is asynchronous on the given cudaStream_t (passed as void*), never
+ * synchronises, never allocates on a hot call. Return 0 on success, else a
+ * PS_E* / cudaError_t code; ps_last_error() gives the message (thread-local).
+ */
+#ifndef PARASTEP_B200_H
+#define PARASTEP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* element types of sampler state / noise vectors */
+enum { PS_F64 = 0, PS_F32 = 1, PS_BF16 = 2 };
+
+/* error codes (besides cudaError_t values) */
+enum {
+  PS_OK = 0,
+  PS_EINVAL = 1001,  /* bad argument: maps to DimensionError/ParameterError */
+  PS_ECUDA = 1002,   /* CUDA runtime error */
+  PS_EUNSUP = 1003   /* unsupported dtype/shape combination */
+};
+
+#define PS_MAX_CYCLE 16
+
+/* One reverse step t (schedule.py:102-131): out = (x - c*eps)/sqrt_a
+ * (+ sigma*z_t when noisy). Coefficients are computed on the host in Python
+ * float64 exactly as posterior_mean does (math.sqrt, correctly rounded). */
+typedef struct ps_step {
+  double c;       /* (1 - alpha_t) / sqrt(1 - alpha_bar_t) */
+  double sqrt_a;  /* sqrt(alpha_t) */
+  double sigma;   /* sigma_t */
+  int32_t t;      /* step index, selects z stream (STEP<<32)|t */
+  int32_t noisy;  /* 0 when t == 1 or sigma_mode == "zero" */
+} ps_step;
+
+const char* ps_last_error(void);
+int ps_version(void);
+int ps_sm_count(int device);
+
+/* ---- counter RNG (numerics.py:30-120) ------------------------------------
+ * out[i] = draw at counter counter0+i of (seed, stream). Integer part
+ * (SplitMix64) is bit-exact; uniform() is bit-exact; normal() uses fp64
+ * log/sqrt/sincos (<= 2 ulp from numpy). dtype: PS_F64 or PS_F32. */
+int ps_rng_normal(void* out, int64_t n, uint64_t seed, uint64_t stream, uint64_t counter0,
+                  int dtype, void* cuda_stream);
+/* same, seed read from device memory (CUDA-graph replayable per seed) */
+int ps_rng_normal_dev(void* out, int64_t n, const uint64_t* d_seed, uint64_t stream,
+                      uint64_t counter0, int dtype, void* cuda_stream);
+int ps_rng_uniform(void* out, int64_t n, uint64_t seed, uint64_t stream, uint64_t counter0,
+                   int dtype, void* cuda_stream);
+/* Xavier-uniform weight init (predictor.py:202-215): out[i] = (2u_i - 1)*limit */
+int ps_rng_xavier(void* out, int64_t n, uint64_t seed, uint64_t stream, double limit,
+                  int dtype, void* cuda_stream);
+
+/* ---- fused scheduler: the reuse-then-predict round -----------------------
+ * One launch does, per element (chain held in fp64 registers, no FMA
+ * contraction, z_t generated in-register from d_seed):
+ *   1) APPLY: x = x_in; for k < n_apply: rec_x[k] <- x (if non-NULL);
+ *             x = step(x, eps_apply[k], apply[k]);   x_out <- x
+ *      (engines.py:333-336 / worker.py:204, the canonical chain)
+ *   2) ROLL:  for lane j in [lane_lo, lane_hi), j >= 1:
+ *             xj = x; for k < j: xj = step(xj, cache[j], roll[k]); lane_out[j] <- xj
+ *      (engines.py:321-327, lane j rolled with its own cached eps)
+ * n_apply may be 0 (roll only, x = x_in) and lane_hi <= 1 disables the roll.
+ * x_out may alias x_in. Host arrays are copied into the kernel parameters. */
+int ps_sched_cycle(const void* x_in, void* x_out, int64_t n, int dtype,
+                   const uint64_t* d_seed,
+                   int n_apply, const ps_step* host_apply, const void* const* host_eps_apply,
+                   void* const* host_rec_x,
+                   int lane_lo, int lane_hi, const ps_step* host_roll,
+                   const void* const* host_lane_cache, void* const* host_lane_out,
+                   void* cuda_stream);
+
+/* single ddpm_step with caller-supplied noise (z may be NULL when !noisy);
+ * used for bit-exact checks against schedule.ddpm_step. */
+int ps_sched_step_z(const void* x, const void* eps, const void* z, void* out, int64_t n,
+                    int dtype, const ps_step* host_step, void* cuda_stream);
+
+/* ---- reference MLP predictor (predictor.py:133-166), fp64 ----------------
+ * a0 = [x, temb[t]]; z = a W + b; silu/tanh on hidden layers; linear out.
+ * W_l is (fan_in, fan_out) row-major exactly as PredictorWeights stores it.
+ * temb_table: (T+1) x embed_dim rows, row t = time_embed(t, T, E).
+ * B rows (lanes) per call, host_ts[b] is lane b's step. */
+typedef struct ps_mlp {
+  int32_t n_layers;
+  int32_t activation;  /* 0 = tanh, 1 = silu (predictor.py:33-36) */
+  int32_t data_dim;
+  int32_t embed_dim;
+  int32_t dims[17];            /* dims[0] = data_dim + embed_dim ... dims[n_layers] */
+  const double* W[16];
+  const double* b[16];
+  const double* temb_table;
+} ps_mlp;
+
+size_t ps_mlp_workspace_bytes(const ps_mlp* m, int B);
+int ps_mlp_forward(const ps_mlp* m, const double* x, const int32_t* host_ts, int B, double* out,
+                   void* workspace, void* cuda_stream);
+
+/* ---- DiT-shaped predictor (paper_2505_14741_b200/spec.py) ----------------
+ * Opaque handle owning its workspace; weights are device tensors owned by
+ * the caller (created by the Python side with ps_rng_xavier). */
+typedef struct ps_dit_config {
+  int32_t channels, frames, height, width, layout; /* layout 0 = CHW, 1 = FHWC */
+  int32_t patch, hidden, depth, heads, mlp_hidden, freq_dim;
+  int32_t max_batch;
+  int32_t precision;  /* 0 = fp32 (fp32-accurate GEMMs), 1 = bf16 tensor-core */
+  int32_t gemm_impl;  /* 0 = auto, 1 = SIMT fp32, 2 = tcgen05 */
+} ps_dit_config;
+
+/* weight pointer order (fp32, (fan_in, fan_out) row-major, see
+ * spec.layer_table): W[i], b[i] for i < n_layers; plus pos table (L x D) and
+ * frequency table ((T+1) x freq_dim) */
+typedef struct ps_dit_weights {
+  int32_t n_layers;
+  const float* const* W;
+  const float* const* b;
+  const float* pos;
+  const float* freq_table;
+  int32_t freq_rows;
+} ps_dit_weights;
+
+typedef struct ps_dit ps_dit;
+int ps_dit_create(const ps_dit_config* cfg, const ps_dit_weights* w, ps_dit** out);
+int ps_dit_forward(ps_dit* h, const float* x, const int32_t* host_ts, int B, float* eps_out,
+                   void* cuda_stream);
+int ps_dit_destroy(ps_dit* h);
+/* algorithmic FLOPs of one forward of one sample (GEMMs + attention) */
+double ps_dit_flops(const ps_dit* h);
+
+/* Diagnostic (allocates + synchronises; never on the hot path):
+ * C[M,N] = A[M,K] W[K,N] + bias with fp32 buffers in the reference layout,
+ * through the tcgen05 kernel (impl 2; precision 1 = bf16, 0 = 3xTF32) or the
+ * SIMT fp32 kernel (impl 1). */
+int ps_gemm_test(const float* A, const float* W, const float* bias, float* C, int M, int N, int K,
+                 int precision, int impl, void* cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PARASTEP_B200_H */

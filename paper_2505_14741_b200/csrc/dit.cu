@@ -1,0 +1,324 @@
+// DiT-shaped noise predictor: handle, workspace, forward orchestration.
+// Architecture pinned in paper_2505_14741_b200/spec.py; the CPU oracle is
+// oracle/dit.py. One forward = ~7 launches per block; the engine captures a
+// whole denoise run into one CUDA graph, so launch latency is paid once.
+
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "gemm_simt.cuh"
+#include "gemm_tc.cuh"
+
+using namespace ps;
+
+struct BlockW {
+  const float *ada, *qkv, *proj, *fc1, *fc2;
+  const float *b_ada, *b_qkv, *b_proj, *b_fc1, *b_fc2;
+};
+
+struct ps_dit {
+  ps_dit_config cfg;
+  DitGeom g;
+  int L, D, H, dh, Dm, P, depth, freq_dim, n_ada;
+  int64_t n_latent;
+  const float *Wpe, *bpe, *Wt1, *bt1, *Wt2, *bt2, *Wfa, *bfa, *Wfo, *bfo;
+  std::vector<BlockW> blk;
+  const float *pos, *freq;
+  int freq_rows;
+  // owned device memory
+  std::vector<void*> owned;
+  float *Wada_all, *bada_all;
+  float *h, *a, *qkv, *o, *hid, *t1, *silu_c, *mod;
+  // tensor-core operand copies (gemm_tc.cuh)
+  TcWeights tcw;
+  TcActs tca;
+  bool use_tc;
+  double flops;
+};
+
+static int dalloc(ps_dit* h, void** p, size_t bytes) {
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) return fail((int)e, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  h->owned.push_back(*p);
+  return 0;
+}
+
+template <typename T>
+static int dalloc_t(ps_dit* h, T** p, size_t count) {
+  return dalloc(h, reinterpret_cast<void**>(p), count * sizeof(T) + 256);
+}
+
+static int gemv(const float* in, int64_t in_stride, const int32_t* rows, const float* W,
+                const float* bias, float* out, int K, int N, int B, int act, cudaStream_t st) {
+  GemvArgs p{};
+  p.in = in;
+  p.in_stride = in_stride;
+  for (int b = 0; b < B; ++b) p.in_row[b] = rows ? rows[b] : b;
+  p.W = W;
+  p.bias = bias;
+  p.out = out;
+  p.K = K;
+  p.N = N;
+  p.B = B;
+  p.act = act;
+  gemv_kernel<<<(N + GV_COLS - 1) / GV_COLS, GV_COLS * GV_KGRP, 0, st>>>(p);
+  return check_launch("gemv");
+}
+
+static int ln_mod(ps_dit* h, int rows, int shift_off, int scale_off, const TcOperand* dst,
+                  cudaStream_t st) {
+  LnModArgs p{};
+  p.h = h->h;
+  p.rows = rows;
+  p.D = h->D;
+  p.L = h->L;
+  p.mod = h->mod;
+  p.mod_stride = h->n_ada;
+  p.shift_off = shift_off;
+  p.scale_off = scale_off;
+  if (dst) {
+    p.out_bf16 = dst->bf16;
+    p.out_hi = dst->hi;
+    p.out_lo = dst->lo;
+    p.out_f32 = dst->f32;
+  } else {
+    p.out_f32 = h->a;
+  }
+  const int threads = 256;
+  ln_mod_kernel<<<(rows * 32 + threads - 1) / threads, threads, 0, st>>>(p);
+  return check_launch("ln_mod");
+}
+
+// GEMM dispatch: layer weights W (K, N) fp32 reference layout; `tc` selects
+// the tensor-core copy index. A is either h->a-style fp32 (SIMT) or a
+// TcOperand (tensor core).
+static int gemm(ps_dit* h, int tc_layer, const float* A_f32, const TcOperand* A_tc, const float* W,
+                int M, int N, int K, const Epi& e, cudaStream_t st) {
+  if (h->use_tc) return tc_gemm(h->tcw, tc_layer, *A_tc, M, N, K, e, h->cfg.precision, st);
+  dim3 grid((N + SG_BN - 1) / SG_BN, (M + SG_BM - 1) / SG_BM);
+  gemm_simt_kernel<<<grid, 256, 0, st>>>(A_f32, W, M, N, K, e);
+  return check_launch("gemm_simt");
+}
+
+extern "C" {
+
+int ps_dit_create(const ps_dit_config* cfg, const ps_dit_weights* w, ps_dit** out) {
+  PS_CHECK_ARG(cfg && w && out, "null argument");
+  const int D = cfg->hidden, depth = cfg->depth;
+  PS_CHECK_ARG(D % cfg->heads == 0, "hidden % heads != 0");
+  PS_CHECK_ARG(D / cfg->heads <= 32 * AT_MAXU, "head_dim > 128 unsupported");
+  PS_CHECK_ARG(cfg->max_batch >= 1 && cfg->max_batch <= GV_MAXB, "max_batch must be in [1, 16]");
+  PS_CHECK_ARG(w->n_layers == 3 + 5 * depth + 2, "weight count does not match depth");
+  ps_dit* h = new ps_dit();
+  h->cfg = *cfg;
+  h->D = D;
+  h->depth = depth;
+  h->H = cfg->heads;
+  h->dh = D / cfg->heads;
+  h->Dm = cfg->mlp_hidden;
+  h->P = cfg->channels * cfg->patch * cfg->patch;
+  h->freq_dim = cfg->freq_dim;
+  h->g.C = cfg->channels;
+  h->g.F = cfg->frames;
+  h->g.H = cfg->height;
+  h->g.W = cfg->width;
+  h->g.layout = cfg->layout;
+  h->g.p = cfg->patch;
+  h->g.D = D;
+  h->g.gh = cfg->height / cfg->patch;
+  h->g.gw = cfg->width / cfg->patch;
+  h->L = h->g.L = cfg->frames * h->g.gh * h->g.gw;
+  h->n_latent = (int64_t)cfg->channels * cfg->frames * cfg->height * cfg->width;
+  h->n_ada = depth * 6 * D + 2 * D;
+  int li = 0;
+  h->Wpe = w->W[li]; h->bpe = w->b[li++];
+  h->Wt1 = w->W[li]; h->bt1 = w->b[li++];
+  h->Wt2 = w->W[li]; h->bt2 = w->b[li++];
+  h->blk.resize(depth);
+  for (int i = 0; i < depth; ++i) {
+    BlockW& bw = h->blk[i];
+    bw.ada = w->W[li]; bw.b_ada = w->b[li++];
+    bw.qkv = w->W[li]; bw.b_qkv = w->b[li++];
+    bw.proj = w->W[li]; bw.b_proj = w->b[li++];
+    bw.fc1 = w->W[li]; bw.b_fc1 = w->b[li++];
+    bw.fc2 = w->W[li]; bw.b_fc2 = w->b[li++];
+  }
+  h->Wfa = w->W[li]; h->bfa = w->b[li++];
+  h->Wfo = w->W[li]; h->bfo = w->b[li++];
+  h->pos = w->pos;
+  h->freq = w->freq_table;
+  h->freq_rows = w->freq_rows;
+
+  const int B = cfg->max_batch;
+  const size_t BL = (size_t)B * h->L;
+  int rc = 0;
+  if ((rc = dalloc_t(h, &h->Wada_all, (size_t)D * h->n_ada)) ||
+      (rc = dalloc_t(h, &h->bada_all, (size_t)h->n_ada)) ||
+      (rc = dalloc_t(h, &h->h, BL * D)) || (rc = dalloc_t(h, &h->a, BL * D)) ||
+      (rc = dalloc_t(h, &h->qkv, BL * 3 * D)) || (rc = dalloc_t(h, &h->o, BL * D)) ||
+      (rc = dalloc_t(h, &h->hid, BL * h->Dm)) || (rc = dalloc_t(h, &h->t1, (size_t)B * D)) ||
+      (rc = dalloc_t(h, &h->silu_c, (size_t)B * D)) ||
+      (rc = dalloc_t(h, &h->mod, (size_t)B * h->n_ada))) {
+    ps_dit_destroy(h);
+    return rc;
+  }
+  // concatenate every adaLN projection into one (D, n_ada) matrix so the
+  // whole per-forward conditioning is a single GEMV launch
+  for (int i = 0; i <= depth; ++i) {
+    const float* src = i < depth ? h->blk[i].ada : h->Wfa;
+    const float* bsrc = i < depth ? h->blk[i].b_ada : h->bfa;
+    const int cols = i < depth ? 6 * D : 2 * D;
+    const size_t off = (size_t)i * 6 * D;
+    cudaError_t e = cudaMemcpy2D(h->Wada_all + off, (size_t)h->n_ada * sizeof(float), src,
+                                 (size_t)cols * sizeof(float), (size_t)cols * sizeof(float), D,
+                                 cudaMemcpyDeviceToDevice);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(h->bada_all + off, bsrc, cols * sizeof(float), cudaMemcpyDeviceToDevice);
+    if (e != cudaSuccess) {
+      ps_dit_destroy(h);
+      return fail((int)e, std::string("ada concat: ") + cudaGetErrorString(e));
+    }
+  }
+  const int impl = cfg->gemm_impl;
+  h->use_tc = (impl == 2) || (impl == 0 && cfg->precision == 1);
+  if (cfg->precision == 1 && !h->use_tc) {
+    ps_dit_destroy(h);
+    return fail(PS_EUNSUP, "bf16 precision needs the tensor-core GEMM");
+  }
+  if (h->use_tc) {
+    std::vector<const float*> Ws;
+    std::vector<int> Ks, Ns;
+    for (int i = 0; i < depth; ++i) {
+      const BlockW& bw = h->blk[i];
+      Ws.push_back(bw.qkv); Ks.push_back(D); Ns.push_back(3 * D);
+      Ws.push_back(bw.proj); Ks.push_back(D); Ns.push_back(D);
+      Ws.push_back(bw.fc1); Ks.push_back(D); Ns.push_back(h->Dm);
+      Ws.push_back(bw.fc2); Ks.push_back(h->Dm); Ns.push_back(D);
+    }
+    Ws.push_back(h->Wfo); Ks.push_back(D); Ns.push_back(h->P);
+    rc = tc_prepare(h->tcw, h->tca, Ws, Ks, Ns, (int)BL, D, h->Dm, cfg->precision);
+    if (rc) {
+      ps_dit_destroy(h);
+      return rc;
+    }
+  }
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    ps_dit_destroy(h);
+    return fail((int)e, std::string("dit create: ") + cudaGetErrorString(e));
+  }
+  const double Lf = h->L;
+  h->flops = 2.0 * (Lf * h->P * D + depth * Lf * D * (4.0 * D + 2.0 * h->Dm) + Lf * D * h->P +
+                    depth * 2.0 * Lf * Lf * D);
+  *out = h;
+  return 0;
+}
+
+double ps_dit_flops(const ps_dit* h) { return h ? h->flops : 0.0; }
+
+int ps_dit_destroy(ps_dit* h) {
+  if (!h) return 0;
+  tc_release(h->tcw, h->tca);
+  for (void* p : h->owned) cudaFree(p);
+  delete h;
+  return 0;
+}
+
+int ps_dit_forward(ps_dit* h, const float* x, const int32_t* host_ts, int B, float* eps_out,
+                   void* cs) {
+  PS_CHECK_ARG(h && x && host_ts && eps_out, "null argument");
+  PS_CHECK_ARG(B >= 1 && B <= h->cfg.max_batch, "batch exceeds max_batch");
+  for (int b = 0; b < B; ++b)
+    PS_CHECK_ARG(host_ts[b] >= 0 && host_ts[b] < h->freq_rows, "step index outside [0, T]");
+  cudaStream_t st = as_stream(cs);
+  const int D = h->D, L = h->L, M = B * L;
+  int rc;
+  // conditioning: c = temb2(silu(temb1(freq[t]))), all adaLN vectors at once
+  if ((rc = gemv(h->freq, h->freq_dim, host_ts, h->Wt1, h->bt1, h->t1, h->freq_dim, D, B, 1, st)))
+    return rc;
+  if ((rc = gemv(h->t1, D, nullptr, h->Wt2, h->bt2, h->silu_c, D, D, B, 1, st))) return rc;
+  if ((rc = gemv(h->silu_c, D, nullptr, h->Wada_all, h->bada_all, h->mod, D, h->n_ada, B, 0, st)))
+    return rc;
+  patch_embed_kernel<<<M, 128, h->P * sizeof(float), st>>>(x, h->n_latent, h->g, h->P, h->Wpe,
+                                                           h->bpe, h->pos, h->h, B);
+  if ((rc = check_launch("patch_embed"))) return rc;
+
+  const TcOperand* aop = h->use_tc ? &h->tca.a : nullptr;
+  const TcOperand* oop = h->use_tc ? &h->tca.o : nullptr;
+  const TcOperand* hop = h->use_tc ? &h->tca.hid : nullptr;
+  AttnArgs at{};
+  at.qkv = h->qkv;
+  at.L = L;
+  at.D = D;
+  at.H = h->H;
+  at.dh = h->dh;
+  at.scale = 1.0f / sqrtf((float)h->dh);
+  if (h->use_tc) {
+    at.out_bf16 = h->tca.o.bf16;
+    at.out_hi = h->tca.o.hi;
+    at.out_lo = h->tca.o.lo;
+    at.out_f32 = h->tca.o.f32;
+  } else {
+    at.out_f32 = h->o;
+  }
+  const size_t at_smem = (size_t)(AT_K * (h->dh + 1) + AT_K * h->dh + AT_Q * h->dh) * sizeof(float);
+  static bool at_attr = false;
+  if (!at_attr) {
+    cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    at_attr = true;
+  }
+  for (int i = 0; i < h->depth; ++i) {
+    const BlockW& bw = h->blk[i];
+    const int base = i * 6 * D;
+    if ((rc = ln_mod(h, M, base, base + D, aop, st))) return rc;
+    Epi e{};
+    e.mode = EPI_STORE;
+    e.bias = bw.b_qkv;
+    e.out = h->qkv;
+    if ((rc = gemm(h, 4 * i + 0, h->a, aop, bw.qkv, M, 3 * D, D, e, st))) return rc;
+    dim3 ag((L + AT_Q - 1) / AT_Q, h->H, B);
+    attn_kernel<<<ag, AT_WARPS * 32, at_smem, st>>>(at);
+    if ((rc = check_launch("attn"))) return rc;
+    e = Epi{};
+    e.mode = EPI_RESID;
+    e.bias = bw.b_proj;
+    e.resid = h->h;
+    e.gate = h->mod + base + 2 * D;
+    e.gate_stride = h->n_ada;
+    e.L = L;
+    if ((rc = gemm(h, 4 * i + 1, h->o, oop, bw.proj, M, D, D, e, st))) return rc;
+    if ((rc = ln_mod(h, M, base + 3 * D, base + 4 * D, aop, st))) return rc;
+    e = Epi{};
+    e.mode = EPI_GELU;
+    e.bias = bw.b_fc1;
+    if (h->use_tc) {
+      e.out = h->tca.hid.f32;
+      e.out_bf16 = h->tca.hid.bf16;
+      e.out_hi = h->tca.hid.hi;
+      e.out_lo = h->tca.hid.lo;
+    } else {
+      e.out = h->hid;
+    }
+    if ((rc = gemm(h, 4 * i + 2, h->a, aop, bw.fc1, M, h->Dm, D, e, st))) return rc;
+    e = Epi{};
+    e.mode = EPI_RESID;
+    e.bias = bw.b_fc2;
+    e.resid = h->h;
+    e.gate = h->mod + base + 5 * D;
+    e.gate_stride = h->n_ada;
+    e.L = L;
+    if ((rc = gemm(h, 4 * i + 3, h->hid, hop, bw.fc2, M, D, h->Dm, e, st))) return rc;
+  }
+  const int fb = h->depth * 6 * D;
+  if ((rc = ln_mod(h, M, fb, fb + D, aop, st))) return rc;
+  Epi e{};
+  e.mode = EPI_UNPATCH;
+  e.bias = h->bfo;
+  e.g = h->g;
+  e.eps = eps_out;
+  e.n_latent = h->n_latent;
+  return gemm(h, 4 * h->depth, h->a, aop, h->Wfo, M, h->P, D, e, st);
+}
+
+}  // extern "C"

@@ -1,0 +1,229 @@
+// Host side of the tcgen05 GEMM: operand preparation, TMA descriptors,
+// launch; plus a C-ABI test entry that runs one GEMM against caller buffers.
+
+#include <cstring>
+#include <mutex>
+
+#include "gemm_tc.cuh"
+
+namespace ps {
+
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static int get_encode() {
+  if (g_encode) return 0;
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  cudaError_t e = cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000,
+                                                   cudaEnableDefault, &q);
+  if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+    return fail(PS_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return 0;
+}
+
+// 2-D K-major map: dims {K, rows}, box {128 B of K, box_rows}, 128 B swizzle
+static int make_map(CUtensorMap* m, const void* base, int esz, int K, int rows, int box_rows) {
+  if (int rc = get_encode()) return rc;
+  CUtensorMapDataType dt =
+      esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)K * esz};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / esz), (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PS_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return 0;
+}
+
+// W (K, N) fp32 row-major -> Wt [N][K] as bf16, or as the tf32 hi/lo pair
+__global__ void transpose_convert_kernel(const float* __restrict__ W, int K, int N,
+                                         __nv_bfloat16* out_bf16, float* out_hi, float* out_lo) {
+  __shared__ float tile[32][33];
+  const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int k = k0 + r, n = n0 + threadIdx.x;
+    tile[r][threadIdx.x] = (k < K && n < N) ? W[(int64_t)k * N + n] : 0.f;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int n = n0 + r, k = k0 + threadIdx.x;
+    if (n < N && k < K) {
+      const float v = tile[threadIdx.x][r];
+      const int64_t idx = (int64_t)n * K + k;
+      if (out_bf16) out_bf16[idx] = __float2bfloat16_rn(v);
+      if (out_hi) {
+        const float hi = tf32_hi(v);
+        out_hi[idx] = hi;
+        out_lo[idx] = v - hi;
+      }
+    }
+  }
+}
+
+static int alloc_operand(TcActs& acts, TcOperand& op, int rows, int cols, int precision) {
+  op.rows = rows;
+  op.cols = cols;
+  const size_t n = (size_t)rows * cols;
+  cudaError_t e;
+  if (precision == 1) {
+    e = cudaMalloc(&op.bf16, n * 2);
+    if (e != cudaSuccess) return fail((int)e, "cudaMalloc operand");
+    acts.owned.push_back(op.bf16);
+    cudaMemset(op.bf16, 0, n * 2);
+    return make_map(&op.map_main, op.bf16, 2, cols, rows, TC_BM);
+  }
+  e = cudaMalloc(&op.hi, n * 4);
+  if (e == cudaSuccess) {
+    acts.owned.push_back(op.hi);
+    e = cudaMalloc(&op.lo, n * 4);
+  }
+  if (e != cudaSuccess) return fail((int)e, "cudaMalloc operand");
+  acts.owned.push_back(op.lo);
+  cudaMemset(op.hi, 0, n * 4);
+  cudaMemset(op.lo, 0, n * 4);
+  if (int rc = make_map(&op.map_main, op.hi, 4, cols, rows, TC_BM)) return rc;
+  return make_map(&op.map_lo, op.lo, 4, cols, rows, TC_BM);
+}
+
+static int bn_for(int precision, int M) { return (precision == 1 && M > 1024) ? 128 : 64; }
+
+template <int KIND, int BN>
+static int launch(const TcLayer& L, const TcOperand& A, int M, int N, int K, const Epi& e,
+                  cudaStream_t st) {
+  using C = TcCfg<KIND, BN>;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(gemm_tc_kernel<KIND, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         C::SMEM);
+  });
+  dim3 grid((N + BN - 1) / BN, (M + TC_BM - 1) / TC_BM);
+  const CUtensorMap& mb = (BN == 128) ? L.map_lo : L.map_main;  // see tc_prepare (bf16 only)
+  if (KIND == KIND_BF16)
+    gemm_tc_kernel<KIND, BN><<<grid, TC_THREADS, C::SMEM, st>>>(A.map_main, A.map_main, mb, mb, M,
+                                                                 N, K, e);
+  else
+    gemm_tc_kernel<KIND, BN><<<grid, TC_THREADS, C::SMEM, st>>>(A.map_main, A.map_lo, L.map_main,
+                                                                 L.map_lo, M, N, K, e);
+  return check_launch("gemm_tc");
+}
+
+int tc_prepare(TcWeights& w, TcActs& acts, const std::vector<const float*>& Ws,
+               const std::vector<int>& Ks, const std::vector<int>& Ns, int max_rows, int D, int Dm,
+               int precision) {
+  w.precision = precision;
+  w.layers.resize(Ws.size());
+  for (size_t i = 0; i < Ws.size(); ++i) {
+    TcLayer& L = w.layers[i];
+    L.K = Ks[i];
+    L.N = Ns[i];
+    const size_t n = (size_t)L.K * L.N;
+    PS_CHECK_ARG(L.K % 8 == 0, "tensor-core GEMM needs K % 8 == 0");
+    cudaError_t e;
+    if (precision == 1) {
+      e = cudaMalloc(&L.w_main, n * 2);
+      if (e != cudaSuccess) return fail((int)e, "cudaMalloc weights");
+    } else {
+      e = cudaMalloc(&L.w_main, n * 4);
+      if (e == cudaSuccess) e = cudaMalloc(&L.w_lo, n * 4);
+      if (e != cudaSuccess) return fail((int)e, "cudaMalloc weights");
+    }
+    dim3 grid((L.N + 31) / 32, (L.K + 31) / 32), blk(32, 8);
+    transpose_convert_kernel<<<grid, blk>>>(
+        Ws[i], L.K, L.N, precision == 1 ? (__nv_bfloat16*)L.w_main : nullptr,
+        precision == 1 ? nullptr : (float*)L.w_main, precision == 1 ? nullptr : (float*)L.w_lo);
+    if (int rc = check_launch("transpose_convert")) return rc;
+    if (precision == 1) {
+      // bf16: map_main boxes 64 rows of N, map_lo (reused slot) boxes 128
+      if (int rc = make_map(&L.map_main, L.w_main, 2, L.K, L.N, 64)) return rc;
+      if (int rc = make_map(&L.map_lo, L.w_main, 2, L.K, L.N, 128)) return rc;
+    } else {
+      if (int rc = make_map(&L.map_main, L.w_main, 4, L.K, L.N, 64)) return rc;
+      if (int rc = make_map(&L.map_lo, L.w_lo, 4, L.K, L.N, 64)) return rc;
+    }
+  }
+  if (int rc = alloc_operand(acts, acts.a, max_rows, D, precision)) return rc;
+  if (int rc = alloc_operand(acts, acts.o, max_rows, D, precision)) return rc;
+  if (int rc = alloc_operand(acts, acts.hid, max_rows, Dm, precision)) return rc;
+  return 0;
+}
+
+int tc_gemm(const TcWeights& w, int layer, const TcOperand& A, int M, int N, int K, const Epi& e,
+            int precision, cudaStream_t st) {
+  const TcLayer& L = w.layers[layer];
+  if (precision == 1) {
+    if (bn_for(precision, M) == 128) return launch<KIND_BF16, 128>(L, A, M, N, K, e, st);
+    return launch<KIND_BF16, 64>(L, A, M, N, K, e, st);
+  }
+  return launch<KIND_TF32X3, 64>(L, A, M, N, K, e, st);
+}
+
+void tc_release(TcWeights& w, TcActs& acts) {
+  for (auto& L : w.layers) {
+    if (L.w_main) cudaFree(L.w_main);
+    if (L.w_lo) cudaFree(L.w_lo);
+  }
+  w.layers.clear();
+  for (void* p : acts.owned) cudaFree(p);
+  acts.owned.clear();
+}
+
+}  // namespace ps
+
+using namespace ps;
+
+namespace ps {
+__global__ void convert_act_kernel(const float* src, __nv_bfloat16* bf, float* hi, float* lo,
+                                   int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float v = src[i];
+  if (bf) bf[i] = __float2bfloat16_rn(v);
+  if (hi) {
+    const float h = tf32_hi(v);
+    hi[i] = h;
+    lo[i] = v - h;
+  }
+}
+}  // namespace ps
+
+extern "C" {
+
+// Test entry: C[M, N] = A[M, K] W[K, N] (+bias) on the tensor cores
+// (precision 1 = bf16, 0 = 3xTF32) or the SIMT path (impl 1). A and W are
+// fp32 device buffers in the reference layout; C fp32 [M, N]. Allocates and
+// synchronises: test/diagnostic use only, never on the hot path.
+int ps_gemm_test(const float* A, const float* W, const float* bias, float* Cout, int M, int N,
+                 int K, int precision, int impl, void* cs) {
+  PS_CHECK_ARG(M > 0 && N > 0 && K > 0, "bad GEMM shape");
+  cudaStream_t st = as_stream(cs);
+  Epi e{};
+  e.mode = EPI_STORE;
+  e.bias = bias;
+  e.out = Cout;
+  if (impl == 1) {
+    dim3 grid((N + SG_BN - 1) / SG_BN, (M + SG_BM - 1) / SG_BM);
+    gemm_simt_kernel<<<grid, 256, 0, st>>>(A, W, M, N, K, e);
+    return check_launch("gemm_simt");
+  }
+  TcWeights w;
+  TcActs acts;
+  std::vector<const float*> Ws{W};
+  std::vector<int> Ks{K}, Ns{N};
+  int rc = tc_prepare(w, acts, Ws, Ks, Ns, M, K, K, precision);
+  if (!rc) {
+    const int64_t n = (int64_t)M * K;
+    convert_act_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(A, acts.a.bf16, acts.a.hi,
+                                                                    acts.a.lo, n);
+    rc = check_launch("convert_act");
+  }
+  if (!rc) rc = tc_gemm(w, 0, acts.a, M, N, K, e, precision, st);
+  cudaError_t se = cudaStreamSynchronize(st);
+  if (!rc && se != cudaSuccess) rc = fail((int)se, std::string("gemm_test: ") + cudaGetErrorString(se));
+  tc_release(w, acts);
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,294 @@
+// tcgen05 tensor-core GEMM for the DiT predictor (sm_100a).
+//
+//   C[M, N] = A[M, K] x W[K, N] + bias, fused DiT epilogues (gemm_simt.cuh Epi)
+//
+// Operands are K-major in HBM: A (activations) row-major [M][K] exactly as
+// the producing kernel (LN-modulate / attention / GELU epilogue) writes it;
+// W is transposed once at load into [N][K]. Per CTA tile 128 x BN:
+//   warp 0 (1 thread)  TMA producer: 128-byte-swizzled K slabs -> smem ring
+//   warp 1 (1 thread)  MMA issuer:   tcgen05.mma, accumulator in TMEM
+//   warp 2             TMEM allocator
+//   warps 0-3          epilogue:     tcgen05.ld -> registers -> fused store
+// Two precisions:
+//   KIND_BF16  kind::f16, bf16 x bf16 -> fp32 (configs[2], DiT-XL/2 bf16)
+//   KIND_TF32X3 kind::tf32 with the 3-pass split a = a_hi + a_lo:
+//              a_hi*b_hi + a_hi*b_lo + a_lo*b_hi  (~fp32 accuracy for the
+//              1e-4 fp32 path, configs[1]); producers write a_hi/a_lo.
+#pragma once
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <vector>
+
+#include "gemm_simt.cuh"
+
+namespace ps {
+
+enum { KIND_BF16 = 0, KIND_TF32X3 = 1 };
+
+struct TcOperand {
+  float* f32 = nullptr;
+  __nv_bfloat16* bf16 = nullptr;
+  float* hi = nullptr;
+  float* lo = nullptr;
+  int rows = 0, cols = 0;
+  CUtensorMap map_main;  // bf16 or hi
+  CUtensorMap map_lo;
+};
+
+struct TcActs {
+  TcOperand a, o, hid;
+  std::vector<void*> owned;
+};
+
+struct TcLayer {
+  int K, N;
+  void* w_main = nullptr;  // bf16 [N][K] or tf32-hi fp32 [N][K]
+  void* w_lo = nullptr;    // tf32-lo fp32 [N][K]
+  CUtensorMap map_main, map_lo;
+  int bn;
+};
+
+struct TcWeights {
+  std::vector<TcLayer> layers;
+  int precision = 0;
+};
+
+constexpr int TC_BM = 128;
+constexpr int TC_THREADS = 128;
+constexpr int TC_STAGES = 4;
+
+// ------------------------------------------------------------------ PTX
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x,
+                                            int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// K-major, 128-byte swizzle smem matrix descriptor (tcgen05 "shared memory
+// descriptor"): start>>4 [0,14), LBO>>4 [16,30) (unused for swizzled K-major,
+// 1), SBO>>4 [32,46) = 1024 B between 8-row groups, version 1 at [46,48),
+// layout SWIZZLE_128B = 2 at [61,64).
+__device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
+  const uint64_t addr = smem_u32(p);
+  uint64_t d = 0;
+  d |= (addr >> 4) & 0x3FFFull;
+  d |= 1ull << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= 1ull << 46;
+  d |= 2ull << 61;
+  return d;
+}
+
+// instruction descriptor: D fp32, A/B format, both K-major, N>>3, M>>4
+__host__ __device__ constexpr uint32_t make_idesc(int kind, int M, int N) {
+  const uint32_t fmt = kind == KIND_BF16 ? 1u : 2u;  // BF16 = 1, TF32 = 2
+  return (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+
+template <int KIND>
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                     uint32_t idesc, uint32_t accumulate) {
+  if constexpr (KIND == KIND_BF16) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  }
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%"
+      "15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ------------------------------------------------------------------ kernel
+template <int KIND, int BN>
+struct TcCfg {
+  static constexpr int BK_BYTES = 128;
+  static constexpr int ESZ = KIND == KIND_BF16 ? 2 : 4;
+  static constexpr int BK = BK_BYTES / ESZ;            // K elements per stage
+  static constexpr int UK = KIND == KIND_BF16 ? 16 : 8;  // K per MMA
+  static constexpr int A_BYTES = TC_BM * BK_BYTES;
+  static constexpr int B_BYTES = BN * BK_BYTES;
+  static constexpr int NOPS = KIND == KIND_BF16 ? 1 : 2;  // main (+lo) copies
+  static constexpr int STAGE_BYTES = NOPS * (A_BYTES + B_BYTES);
+  static constexpr int SMEM = TC_STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
+};
+
+template <int KIND, int BN>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapAlo,
+                   const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapBlo,
+                   int M, int N, int K, const __grid_constant__ Epi e) {
+  using C = TcCfg<KIND, BN>;
+  extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TC_STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + TC_STAGES;
+  uint64_t* accum = empty + TC_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * BN;
+  const int nk = (K + C::BK - 1) / C::BK;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&mapA);
+    tma_prefetch_desc(&mapB);
+    if (KIND == KIND_TF32X3) {
+      tma_prefetch_desc(&mapAlo);
+      tma_prefetch_desc(&mapBlo);
+    }
+    for (int s = 0; s < TC_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accum, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % TC_STAGES;
+      mbar_wait(&empty[s], ((kb / TC_STAGES) & 1) ^ 1);
+      uint8_t* st = smem + s * C::STAGE_BYTES;
+      mbar_expect_tx(&full[s], C::STAGE_BYTES);
+      const int kx = kb * C::BK;
+      tma_load_2d(st, &mapA, &full[s], kx, m0);
+      tma_load_2d(st + C::A_BYTES, &mapB, &full[s], kx, n0);
+      if (KIND == KIND_TF32X3) {
+        tma_load_2d(st + C::A_BYTES + C::B_BYTES, &mapAlo, &full[s], kx, m0);
+        tma_load_2d(st + 2 * C::A_BYTES + C::B_BYTES, &mapBlo, &full[s], kx, n0);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer
+    constexpr uint32_t idesc = make_idesc(KIND, TC_BM, BN);
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % TC_STAGES;
+      mbar_wait(&full[s], (kb / TC_STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint8_t* st = smem + s * C::STAGE_BYTES;
+      const uint64_t a0 = smem_desc_sw128(st);
+      const uint64_t b0 = smem_desc_sw128(st + C::A_BYTES);
+#pragma unroll
+      for (int k = 0; k < C::BK / C::UK; ++k) {
+        // advance 32 B along K inside the swizzle atom: +2 in the >>4 address
+        const uint64_t koff = (uint64_t)(k * C::UK * C::ESZ) >> 4;
+        const uint32_t acc = (kb | k) ? 1u : 0u;
+        umma<KIND>(tmem, a0 + koff, b0 + koff, idesc, acc);
+        if constexpr (KIND == KIND_TF32X3) {
+          const uint64_t alo = smem_desc_sw128(st + C::A_BYTES + C::B_BYTES);
+          const uint64_t blo = smem_desc_sw128(st + 2 * C::A_BYTES + C::B_BYTES);
+          umma<KIND>(tmem, a0 + koff, blo + koff, idesc, 1u);
+          umma<KIND>(tmem, alo + koff, b0 + koff, idesc, 1u);
+        }
+      }
+      umma_commit(&empty[s]);
+    }
+    umma_commit(accum);
+  }
+  __syncwarp();
+
+  // ---------------- epilogue: TMEM -> registers -> fused store
+  mbar_wait(accum, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int row = m0 + warp * 32 + lane;
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll 1
+  for (int c = 0; c < BN; c += 16) {
+    float v[16];
+    tmem_ld16(trow + c, v);
+    if (row < M) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int n = n0 + c + j;
+        if (n < N) epi_store(e, row, n, N, v[j]);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(C::TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------------------ host side
+int tc_prepare(TcWeights& w, TcActs& acts, const std::vector<const float*>& Ws,
+               const std::vector<int>& Ks, const std::vector<int>& Ns, int max_rows, int D, int Dm,
+               int precision);
+int tc_gemm(const TcWeights& w, int layer, const TcOperand& A, int M, int N, int K, const Epi& e,
+            int precision, cudaStream_t st);
+void tc_release(TcWeights& w, TcActs& acts);
+// standalone test entry (C-ABI wrapper in gemm_tc.cu)
+}  // namespace ps

@@ -1,0 +1,330 @@
+// The reuse-then-predict round on device: counter RNG, fused apply+roll.
+//
+// Reference semantics: numerics.py:56-120 (RNG), schedule.py:102-131
+// (ddpm_step), engines.py:299-337 (cycle runner: roll lanes with their own
+// cached eps, apply the fresh eps in round order).
+//
+// Layout: every sampler vector is a flat 1-D latent of n elements (fp64 or
+// fp32), the same flatten order as the reference's numpy vector, so the RNG
+// counter of element i is i. A thread owns VEC consecutive elements (16 B:
+// 2 x fp64 or 4 x fp32) = 1 or 2 Box-Muller pairs, so both normals of a pair
+// are produced by one log/sqrt/sincos. The per-element chain is kept in fp64
+// registers for the whole launch (apply steps, then each lane's roll), so
+// one launch reads x + c eps (+ lane caches) and writes x + lanes: the
+// minimum traffic for the round.
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace ps {
+
+static thread_local std::string g_err;
+void set_error(const std::string& m) { g_err = m; }
+int fail(int code, const std::string& m) {
+  g_err = m;
+  return code;
+}
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail((int)e, std::string(what) + ": " + cudaGetErrorString(e));
+  return 0;
+}
+
+struct CycleParams {
+  const void* x_in;
+  void* x_out;
+  int64_t n;
+  const uint64_t* seed;
+  int n_apply;
+  int lane_lo, lane_hi;
+  ps_step apply[PS_MAX_CYCLE];
+  ps_step roll[PS_MAX_CYCLE];
+  const void* eps[PS_MAX_CYCLE];
+  void* rec[PS_MAX_CYCLE];
+  const void* cache[PS_MAX_CYCLE];
+  void* lane_out[PS_MAX_CYCLE];
+};
+
+template <typename T, int VEC, bool SCALAR = false>
+struct Vec {
+  double v[VEC];
+  __device__ __forceinline__ void load(const void* base, int64_t i0, int cnt) {
+    const T* p = reinterpret_cast<const T*>(base) + i0;
+    if (!SCALAR && cnt == VEC) {
+      if constexpr (sizeof(T) == 4 && VEC == 4) {
+        float4 f = *reinterpret_cast<const float4*>(p);
+        v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+        return;
+      } else if constexpr (sizeof(T) == 8 && VEC == 2) {
+        double2 f = *reinterpret_cast<const double2*>(p);
+        v[0] = f.x; v[1] = f.y;
+        return;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) v[k] = (k < cnt) ? Io<T>::ld(p + k) : 0.0;
+  }
+  __device__ __forceinline__ void store(void* base, int64_t i0, int cnt) const {
+    T* p = reinterpret_cast<T*>(base) + i0;
+    if (!SCALAR && cnt == VEC) {
+      if constexpr (sizeof(T) == 4 && VEC == 4) {
+        *reinterpret_cast<float4*>(p) =
+            make_float4((float)v[0], (float)v[1], (float)v[2], (float)v[3]);
+        return;
+      } else if constexpr (sizeof(T) == 8 && VEC == 2) {
+        *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+        return;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < VEC; ++k)
+      if (k < cnt) Io<T>::st(p + k, v[k]);
+  }
+};
+
+// z_t for VEC consecutive elements starting at even i0 (VEC even)
+template <int VEC>
+__device__ __forceinline__ void gen_z(uint64_t seed, int t, int64_t i0, double* z) {
+  const uint64_t key = stream_key(seed, step_stream(t));
+#pragma unroll
+  for (int q = 0; q < VEC / 2; ++q) normal_pair(key, (uint64_t)(i0 + 2 * q), z[2 * q], z[2 * q + 1]);
+}
+
+template <typename T, int VEC, bool S>
+__device__ __forceinline__ void step_vec(Vec<T, VEC, S>& x, const Vec<T, VEC, S>& e, const ps_step& s,
+                                         const double* z) {
+#pragma unroll
+  for (int k = 0; k < VEC; ++k)
+    x.v[k] = s.noisy ? ddpm_z(x.v[k], e.v[k], s.c, s.sqrt_a, s.sigma, z[k])
+                     : ddpm(x.v[k], e.v[k], s.c, s.sqrt_a);
+}
+
+constexpr int ZCACHE = 7;  // roll steps whose z stays in registers (degree <= 8)
+
+template <typename T, int VEC, bool SCALAR>
+__global__ void __launch_bounds__(256) cycle_kernel(const __grid_constant__ CycleParams p) {
+  const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * VEC;
+  if (i0 >= p.n) return;
+  const int cnt = (p.n - i0) < VEC ? (int)(p.n - i0) : VEC;
+  const uint64_t seed = *p.seed;
+
+  Vec<T, VEC, SCALAR> x;
+  x.load(p.x_in, i0, cnt);
+  double z[VEC];
+  for (int k = 0; k < p.n_apply; ++k) {
+    const ps_step s = p.apply[k];
+    if (p.rec[k]) x.store(p.rec[k], i0, cnt);
+    Vec<T, VEC, SCALAR> e;
+    e.load(p.eps[k], i0, cnt);
+    if (s.noisy) gen_z<VEC>(seed, s.t, i0, z);
+    step_vec(x, e, s, z);
+  }
+  if (p.n_apply > 0) x.store(p.x_out, i0, cnt);
+
+  if (p.lane_hi > 1) {
+    const int nz = p.lane_hi - 1;  // lane j needs roll steps 0..j-1
+    double zc[ZCACHE][VEC];
+#pragma unroll
+    for (int k = 0; k < ZCACHE; ++k)
+      if (k < nz && p.roll[k].noisy) gen_z<VEC>(seed, p.roll[k].t, i0, zc[k]);
+    for (int j = max(p.lane_lo, 1); j < p.lane_hi; ++j) {
+      Vec<T, VEC, SCALAR> c, xj = x;
+      c.load(p.cache[j], i0, cnt);
+#pragma unroll
+      for (int k = 0; k < ZCACHE; ++k)
+        if (k < j) step_vec(xj, c, p.roll[k], zc[k]);
+      for (int k = ZCACHE; k < j; ++k) {
+        if (p.roll[k].noisy) gen_z<VEC>(seed, p.roll[k].t, i0, z);
+        step_vec(xj, c, p.roll[k], z);
+      }
+      xj.store(p.lane_out[j], i0, cnt);
+    }
+  }
+}
+
+template <typename T>
+__global__ void step_z_kernel(const T* x, const T* e, const T* z, T* out, int64_t n, ps_step s) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double xv = Io<T>::ld(x + i), ev = Io<T>::ld(e + i);
+  double r = s.noisy ? ddpm_z(xv, ev, s.c, s.sqrt_a, s.sigma, Io<T>::ld(z + i))
+                     : ddpm(xv, ev, s.c, s.sqrt_a);
+  Io<T>::st(out + i, r);
+}
+
+// one thread per Box-Muller pair
+template <typename T>
+__global__ void rng_normal_kernel(T* out, int64_t n, uint64_t key, uint64_t c0,
+                                  const uint64_t* d_seed, uint64_t stream) {
+  if (d_seed) key = stream_key(*d_seed, stream);  // graph-replayable seed
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // pair slot
+  // element i = c0-relative; pair base counter b = (c0 + i) & ~1
+  const uint64_t first_b = c0 & ~1ull;
+  uint64_t b = first_b + 2ull * (uint64_t)j;
+  int64_t i_even = (int64_t)(b - c0);  // may be -1 when c0 is odd
+  if (i_even >= n) return;
+  double a0, a1;
+  normal_pair(key, b, a0, a1);
+  if (i_even >= 0) Io<T>::st(out + i_even, a0);
+  if (i_even + 1 < n) Io<T>::st(out + i_even + 1, a1);
+}
+
+template <typename T>
+__global__ void rng_uniform_kernel(T* out, int64_t n, uint64_t key, uint64_t c0, double scale,
+                                   int xavier) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double u = uniform_at(key, c0 + (uint64_t)i);
+  // (2u - 1) * limit, rounded like numpy: predictor.py:211
+  Io<T>::st(out + i, xavier ? __dmul_rn(__dsub_rn(__dmul_rn(2.0, u), 1.0), scale) : u);
+}
+
+template <typename T>
+static int launch_cycle(const CycleParams& p, cudaStream_t st, bool vec_ok) {
+  constexpr int VEC = 16 / sizeof(T);
+  if (vec_ok) {
+    int64_t threads = (p.n + VEC - 1) / VEC;
+    unsigned blocks = (unsigned)((threads + 255) / 256);
+    cycle_kernel<T, VEC, false><<<blocks, 256, 0, st>>>(p);
+  } else {
+    // unaligned buffers: 2 elements per thread, scalar loads
+    int64_t threads = (p.n + 1) / 2;
+    unsigned blocks = (unsigned)((threads + 255) / 256);
+    cycle_kernel<T, 2, true><<<blocks, 256, 0, st>>>(p);
+  }
+  return check_launch("cycle_kernel");
+}
+
+}  // namespace ps
+
+using namespace ps;
+
+extern "C" {
+
+const char* ps_last_error(void) { return g_err.c_str(); }
+int ps_version(void) { return 1; }
+
+int ps_sm_count(int device) {
+  int v = 0;
+  PS_TRY(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device));
+  return v;
+}
+
+static int rng_normal(void* out, int64_t n, uint64_t seed, const uint64_t* d_seed,
+                      uint64_t stream, uint64_t counter0, int dtype, void* cs) {
+  PS_CHECK_ARG(n >= 1, "draw count must be >= 1");
+  PS_CHECK_ARG(out != nullptr, "null output");
+  uint64_t key = stream_key(seed, stream);
+  int64_t pairs = (n + 2) / 2 + 1;
+  unsigned blocks = (unsigned)((pairs + 255) / 256);
+  if (dtype == PS_F64)
+    rng_normal_kernel<double><<<blocks, 256, 0, as_stream(cs)>>>((double*)out, n, key, counter0,
+                                                                  d_seed, stream);
+  else if (dtype == PS_F32)
+    rng_normal_kernel<float><<<blocks, 256, 0, as_stream(cs)>>>((float*)out, n, key, counter0,
+                                                                 d_seed, stream);
+  else
+    return fail(PS_EUNSUP, "rng: dtype must be f64 or f32");
+  return check_launch("rng_normal");
+}
+
+int ps_rng_normal(void* out, int64_t n, uint64_t seed, uint64_t stream, uint64_t counter0,
+                  int dtype, void* cs) {
+  return rng_normal(out, n, seed, nullptr, stream, counter0, dtype, cs);
+}
+
+int ps_rng_normal_dev(void* out, int64_t n, const uint64_t* d_seed, uint64_t stream,
+                      uint64_t counter0, int dtype, void* cs) {
+  PS_CHECK_ARG(d_seed != nullptr, "null seed pointer");
+  return rng_normal(out, n, 0, d_seed, stream, counter0, dtype, cs);
+}
+
+static int rng_u(void* out, int64_t n, uint64_t seed, uint64_t stream, uint64_t c0, double scale,
+                 int xavier, int dtype, void* cs) {
+  PS_CHECK_ARG(n >= 1, "draw count must be >= 1");
+  uint64_t key = stream_key(seed, stream);
+  unsigned blocks = (unsigned)((n + 255) / 256);
+  if (dtype == PS_F64)
+    rng_uniform_kernel<double><<<blocks, 256, 0, as_stream(cs)>>>((double*)out, n, key, c0, scale,
+                                                                   xavier);
+  else if (dtype == PS_F32)
+    rng_uniform_kernel<float><<<blocks, 256, 0, as_stream(cs)>>>((float*)out, n, key, c0, scale,
+                                                                  xavier);
+  else
+    return fail(PS_EUNSUP, "rng: dtype must be f64 or f32");
+  return check_launch("rng_uniform");
+}
+
+int ps_rng_uniform(void* out, int64_t n, uint64_t seed, uint64_t stream, uint64_t counter0,
+                   int dtype, void* cs) {
+  return rng_u(out, n, seed, stream, counter0, 1.0, 0, dtype, cs);
+}
+
+int ps_rng_xavier(void* out, int64_t n, uint64_t seed, uint64_t stream, double limit, int dtype,
+                  void* cs) {
+  return rng_u(out, n, seed, stream, 0, limit, 1, dtype, cs);
+}
+
+int ps_sched_cycle(const void* x_in, void* x_out, int64_t n, int dtype, const uint64_t* d_seed,
+                   int n_apply, const ps_step* host_apply, const void* const* host_eps_apply,
+                   void* const* host_rec_x, int lane_lo, int lane_hi, const ps_step* host_roll,
+                   const void* const* host_lane_cache, void* const* host_lane_out, void* cs) {
+  PS_CHECK_ARG(n >= 1, "vector length must be >= 1");
+  PS_CHECK_ARG(d_seed != nullptr, "null seed pointer");
+  PS_CHECK_ARG(n_apply >= 0 && n_apply <= PS_MAX_CYCLE, "n_apply out of range");
+  PS_CHECK_ARG(lane_lo >= 0 && lane_hi <= PS_MAX_CYCLE && (lane_hi <= 1 || lane_lo < lane_hi),
+               "lane range out of range");
+  PS_CHECK_ARG(x_in != nullptr && (n_apply == 0 || x_out != nullptr), "null state pointer");
+  CycleParams p;
+  memset(&p, 0, sizeof(p));
+  p.x_in = x_in;
+  p.x_out = x_out;
+  p.n = n;
+  p.seed = d_seed;
+  p.n_apply = n_apply;
+  p.lane_lo = lane_lo;
+  p.lane_hi = lane_hi;
+  const size_t esz = dtype == PS_F64 ? 8 : 4;
+  bool vec_ok = ((uintptr_t)x_in % 16 == 0) && ((uintptr_t)x_out % 16 == 0);
+  for (int k = 0; k < n_apply; ++k) {
+    p.apply[k] = host_apply[k];
+    p.eps[k] = host_eps_apply[k];
+    PS_CHECK_ARG(p.eps[k] != nullptr, "null eps pointer");
+    p.rec[k] = host_rec_x ? host_rec_x[k] : nullptr;
+    vec_ok = vec_ok && ((uintptr_t)p.eps[k] % 16 == 0) && ((uintptr_t)p.rec[k] % 16 == 0);
+  }
+  if (lane_hi > 1) {
+    for (int k = 0; k < lane_hi - 1; ++k) p.roll[k] = host_roll[k];
+    for (int j = (lane_lo > 1 ? lane_lo : 1); j < lane_hi; ++j) {
+      p.cache[j] = host_lane_cache[j];
+      p.lane_out[j] = host_lane_out[j];
+      PS_CHECK_ARG(p.cache[j] != nullptr && p.lane_out[j] != nullptr, "null lane pointer");
+      vec_ok = vec_ok && ((uintptr_t)p.cache[j] % 16 == 0) && ((uintptr_t)p.lane_out[j] % 16 == 0);
+    }
+  }
+  (void)esz;
+  if (dtype == PS_F64) return launch_cycle<double>(p, as_stream(cs), vec_ok);
+  if (dtype == PS_F32) return launch_cycle<float>(p, as_stream(cs), vec_ok);
+  return fail(PS_EUNSUP, "sched: dtype must be f64 or f32");
+}
+
+int ps_sched_step_z(const void* x, const void* eps, const void* z, void* out, int64_t n,
+                    int dtype, const ps_step* s, void* cs) {
+  PS_CHECK_ARG(n >= 1, "vector length must be >= 1");
+  PS_CHECK_ARG(!s->noisy || z != nullptr, "noisy step needs z");
+  unsigned blocks = (unsigned)((n + 255) / 256);
+  if (dtype == PS_F64)
+    step_z_kernel<double><<<blocks, 256, 0, as_stream(cs)>>>(
+        (const double*)x, (const double*)eps, (const double*)z, (double*)out, n, *s);
+  else if (dtype == PS_F32)
+    step_z_kernel<float><<<blocks, 256, 0, as_stream(cs)>>>(
+        (const float*)x, (const float*)eps, (const float*)z, (float*)out, n, *s);
+  else
+    return fail(PS_EUNSUP, "sched: dtype must be f64 or f32");
+  return check_launch("step_z");
+}
+
+}  // extern "C"

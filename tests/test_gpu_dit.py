@@ -1,0 +1,156 @@
+"""GPU parity of the DiT-shaped predictors and their GEMMs.
+
+Tolerances (stated per the north star): the fp32 path (3xTF32 tcgen05 GEMMs
+or SIMT fp32) must keep x0 within 1e-4 relative MAE of the CPU float64
+oracle driven by the reference sampler (tests/golden/dit_small.npz); the
+bf16 path reports its rel-MAE and is only bounded loosely here.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import core, engines as oeng
+from oracle.dit import DiT as OracleDiT
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2505_14741_b200 import _lib, engines as E, predictor as P  # noqa: E402
+from paper_2505_14741_b200 import schedule as S  # noqa: E402
+from paper_2505_14741_b200.dit import DiTWeights  # noqa: E402
+from paper_2505_14741_b200.spec import SPECS  # noqa: E402
+
+FP32_TOL = 1e-4
+
+
+def _gemm(A, W, bias, precision, impl):
+    lib = _lib.load(require_gpu=True)
+    M, K = A.shape
+    N = W.shape[1]
+    C = torch.zeros((M, N), dtype=torch.float32, device="cuda")
+    _lib.check(lib.ps_gemm_test(_lib.ptr(A), _lib.ptr(W), _lib.ptr(bias), _lib.ptr(C), M, N, K,
+                                precision, impl, _lib.stream_ptr()), "gemm_test")
+    torch.cuda.synchronize()
+    return C
+
+
+@pytest.mark.parametrize("shape", [(256, 1152, 384), (256, 384, 384), (512, 1536, 384),
+                                   (256, 384, 1536), (300, 72, 96), (128, 16, 64),
+                                   (1024, 4608, 1152)])
+@pytest.mark.parametrize("mode", ["tf32x3", "bf16", "simt"])
+def test_gemm_vs_fp64(shape, mode):
+    M, N, K = shape
+    g = torch.Generator(device="cuda").manual_seed(M * N + K)
+    A = torch.randn((M, K), device="cuda", generator=g)
+    W = torch.randn((K, N), device="cuda", generator=g) / K ** 0.5
+    bias = torch.randn(N, device="cuda", generator=g)
+    precision, impl = {"tf32x3": (0, 2), "bf16": (1, 2), "simt": (0, 1)}[mode]
+    C = _gemm(A, W, bias, precision, impl).double()
+    ref = A.double() @ W.double() + bias.double()
+    scale = A.double().abs() @ W.double().abs() + bias.double().abs()
+    err = ((C - ref).abs() / scale).max().item()
+    tol = {"tf32x3": 1e-5, "bf16": 1e-2, "simt": 1e-6}[mode]
+    assert err < tol, (mode, shape, err)
+
+
+def _dit_eps_close(name, bias, precision, impl, tol):
+    spec = SPECS[name]
+    ref = OracleDiT(spec, seed=11, bias_scale=bias)
+    w = DiTWeights(spec, seed=11, precision=precision, bias_scale=bias, gemm_impl=impl,
+                   max_batch=4)
+    rng = np.random.default_rng(1)
+    xs = [rng.standard_normal(spec.data_dim) * s for s in (1.0, 30.0, 300.0)]
+    ts = [20, 7, 1]
+    outs = P.forward_batch(w, xs, ts, 20)
+    errs = []
+    for x, t, o in zip(xs, ts, outs):
+        r = ref(x, t, 20)
+        errs.append(core.rel_mae(r, o))
+        assert np.array_equal(o, P.forward(w, x, t, 20))  # batch == single, bitwise
+    assert max(errs) < tol, (name, precision, impl, errs)
+    return errs
+
+
+@pytest.mark.parametrize("impl", ["simt", "tcgen05"])
+@pytest.mark.parametrize("name,bias", [("dit_tiny", 0.05), ("dit_tiny_video", 0.0),
+                                       ("dit_s2", 0.0)])
+def test_dit_forward_fp32_vs_oracle(name, bias, impl):
+    _dit_eps_close(name, bias, "fp32", impl, 1e-5)
+
+
+@pytest.mark.parametrize("name", ["dit_tiny", "dit_s2"])
+def test_dit_forward_bf16_vs_oracle(name):
+    errs = _dit_eps_close(name, 0.0, "bf16", "tcgen05", 5e-2)
+    print(f"bf16 {name} eps rel-MAE vs fp64 oracle: {errs}")
+
+
+def _traj_close(tr, g, prefix, tol):
+    assert [r.t for r in tr.records] == g[f"{prefix}_t"].tolist()
+    assert [r.fresh for r in tr.records] == g[f"{prefix}_fresh"].tolist()
+    err = core.rel_mae(g[f"{prefix}_x0"], tr.x0)
+    assert err < tol, (prefix, err)
+    if f"{prefix}_x" in g:
+        for k, r in enumerate(tr.records):
+            assert core.rel_mae(g[f"{prefix}_x"][k], r.x) < tol
+            assert core.rel_mae(g[f"{prefix}_eps"][k], r.eps) < tol
+    return err
+
+
+@pytest.mark.parametrize("impl", ["simt", "tcgen05"])
+def test_dit_trajectories_vs_reference_sampler(gold_dit, impl):
+    """The reference's own engines drove the oracle DiT to make these."""
+    for name, bias in (("dit_tiny", 0.05), ("dit_tiny_video", 0.0)):
+        w = DiTWeights(SPECS[name], seed=11, bias_scale=bias, gemm_impl=impl, max_batch=4)
+        for mode in ("posterior", "zero"):
+            sch = S.make_default_schedule(20, mode)
+            n = w.data_dim
+            runs = [("seq", dict(strategy="sequential")),
+                    ("ps2", dict(strategy="parastep", degree=2, warmup=2)),
+                    ("ps3", dict(strategy="parastep", degree=3, warmup=2)),
+                    ("bs4", dict(strategy="batchstep", degree=4, warmup=3))]
+            for tag, kw in runs:
+                cfg = E.RunConfig(steps=20, seed=3, data_dim=n, **kw)
+                _traj_close(E.run_strategy(w, sch, cfg), gold_dit, f"{name}_{mode}_{tag}",
+                            FP32_TOL)
+
+
+@pytest.mark.parametrize("degree", [1, 2, 4, 8])
+def test_dit_s2_fp32_50_steps_within_1e4(degree):
+    """configs[1]: small DiT, 50 deterministic ("DDIM" -> sigma zero) steps,
+    degree d, fp32 on B200 vs the CPU float64 oracle: rel-MAE(x0) <= 1e-4."""
+    spec = SPECS["dit_s2"]
+    w = DiTWeights(spec, seed=0, max_batch=8)
+    sch = S.make_default_schedule(50, "zero")
+    cfg = E.RunConfig(steps=50, warmup=5 if degree > 1 else 0, degree=degree, seed=0,
+                      data_dim=spec.data_dim,
+                      strategy="parastep" if degree > 1 else "sequential")
+    tr = E.run_strategy(w, sch, cfg)
+    ref = OracleDiT(spec, seed=0)
+    osch = core.Sched(50, "zero")
+    if degree == 1:
+        o = oeng.sequential(ref, osch, spec.data_dim, 0)
+    else:
+        o = oeng.cycles(ref, osch, spec.data_dim, 0, warmup=5, degree=degree)
+    err = core.rel_mae(o["x0"], tr.x0)
+    print(f"dit_s2 fp32 d={degree}: rel-MAE(x0) vs fp64 oracle = {err:.3e}")
+    assert err <= FP32_TOL
+
+
+def test_dit_run_deterministic_and_graph():
+    spec = SPECS["dit_tiny"]
+    w = DiTWeights(spec, seed=2, max_batch=4)
+    sch = S.make_default_schedule(20)
+    cfg = E.RunConfig(steps=20, warmup=2, strategy="batchstep", degree=4, seed=9,
+                      data_dim=spec.data_dim)
+    s = E.DeviceSampler(w, sch, cfg)
+    s.run(9)
+    a = s.trajectory()
+    s.run(9, graph=True)
+    b = s.trajectory()
+    assert a.bitwise_equal(b)
+    lanes = E.run_strategy(w, sch, E.RunConfig(steps=20, warmup=2, strategy="parastep", degree=4,
+                                               seed=9, data_dim=spec.data_dim))
+    assert lanes.bitwise_equal(a)

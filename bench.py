@@ -1,0 +1,536 @@
+#!/usr/bin/env python
+"""ParaStep denoise latency on B200 — the BASELINE.json metric.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--impl ours|reference]
+
+One "step" = one complete denoise (T reverse steps) of one synthetic latent
+with the named predictor; at N GPUs it is ParaStep with degree N over NCCL
+(N = 1: the sequential sampler, degree 1). ``value`` = mean denoise latency
+(ms, device time from CUDA events, max over ranks), inputs resident in HBM;
+L2 is flushed (a 512 MiB write) between timed iterations. ``e2e`` = the same
+run through the public sampler API with x_T copied in from pinned host
+memory and the full Trajectory (T x-records, T eps-records, x0) copied back
+and materialised as numpy — the drop-in's user-visible latency.
+
+Default workload (BASELINE.json configs[1]): small random-init DiT
+(DiT-S/2-shaped, spec "dit_s2"), latent 4x32x32, 50 deterministic steps
+("DDIM" -> the reference's sigma_mode="zero"), fp32 path (3xTF32 tcgen05
+GEMMs), warm-up 5 for degree > 1.
+
+``--impl reference`` times the reference's own CPU sampler (pkg/src/parastep,
+installed in baseline/_ref; else the oracle port) driving the oracle DiT
+through its import seam, on rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # BASELINE.json configs[1] (and configs[0]'s workload on the GPU)
+    "small_dit_fp32": dict(spec="dit_s2", precision="fp32", T=50, sigma="zero", warmup=5,
+                           baseline_config=1),
+    # configs[2]
+    "dit_xl2_bf16": dict(spec="dit_xl2", precision="bf16", T=50, sigma="zero", warmup=5,
+                         baseline_config=2),
+    # the reference's own MLP at data_dim 4096 (C1-ref), fp64
+    "c1ref_mlp": dict(spec=None, precision="fp64", T=50, sigma="zero", warmup=5,
+                      baseline_config=0),
+}
+
+L2_FLUSH_BYTES = 512 << 20
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------ helpers
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([c.strip() for c in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._loop, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for nm, v in zip(names, r[3:7]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d["hbm_gbs"], d["bf16_tflops"], "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+def build_predictor(cfg, max_batch):
+    if cfg["spec"] is None:
+        from paper_2505_14741_b200.predictor import TrainConfig, init_weights
+
+        return init_weights(TrainConfig(data_dim=4096, hidden=(64, 64), embed_dim=16, seed=7))
+    from paper_2505_14741_b200.dit import DiTWeights
+
+    return DiTWeights(cfg["spec"], seed=0, precision=cfg["precision"], max_batch=max_batch)
+
+
+def run_cfg(cfg, n, degree, strategy=None):
+    from paper_2505_14741_b200.engines import RunConfig
+
+    if strategy is None:
+        strategy = "sequential" if degree == 1 else "parastep"
+    return RunConfig(steps=cfg["T"], warmup=cfg["warmup"] if degree > 1 else 0,
+                     strategy=strategy, degree=degree, seed=0, data_dim=n)
+
+
+# ------------------------------------------------------------------ CPU reference
+class _StopSample(Exception):
+    pass
+
+
+def reference_module():
+    """The reference package: baseline/_ref (pip --target install) if present."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "parastep")):
+        if ref not in sys.path:
+            sys.path.insert(0, ref)
+        import parastep.engines as RE
+        import parastep.protocol.worker as RW
+        from parastep import commodel, schedule
+
+        return "reference", RE, RW, schedule, commodel
+    return "port", None, None, None, None
+
+
+def cpu_predictor(cfg):
+    from oracle import core
+    from oracle.dit import DiT
+
+    if cfg["spec"] is None:
+        return core.MLP.init(4096, hidden=(64, 64), embed_dim=16, seed=7)
+    from paper_2505_14741_b200.spec import SPECS
+
+    return DiT(SPECS[cfg["spec"]], seed=0)
+
+
+def cpu_reference_run(cfg, max_forwards=None):
+    """Run the reference's sequential sampler on host cores (oracle predictor
+    injected through its import seam, engines.py:40). Returns
+    (elapsed_s, forwards_done, x0 or None, kind)."""
+    import numpy as np
+
+    kind, RE, RW, RS, _ = reference_module()
+    pred = cpu_predictor(cfg)
+    count = [0]
+
+    def fwd(w, x, t, T):
+        if max_forwards is not None and count[0] >= max_forwards:
+            raise _StopSample()
+        count[0] += 1
+        return pred(np.asarray(x, dtype=np.float64), t, T)
+
+    n = pred.data_dim
+    if kind == "reference":
+        class Shim:
+            data_dim = n
+            ballast = 1
+
+        RE.forward = fwd
+        RE.forward_batch = lambda w, xs, ts, T: [fwd(w, x, t, T) for x, t in zip(xs, ts)]
+        RW.forward = fwd
+        sched = RS.make_default_schedule(cfg["T"], cfg["sigma"])
+        rcfg = RE.RunConfig(steps=cfg["T"], seed=0, data_dim=n)
+        t0 = time.perf_counter()
+        try:
+            x0 = RE.run_strategy(Shim(), sched, rcfg).x0
+        except _StopSample:
+            x0 = None
+        return time.perf_counter() - t0, count[0], x0, kind
+    from oracle import core, engines as oeng
+
+    t0 = time.perf_counter()
+    try:
+        x0 = oeng.sequential(lambda x, t, T: fwd(None, x, t, T), core.Sched(cfg["T"], cfg["sigma"]),
+                             n, 0)["x0"]
+    except _StopSample:
+        x0 = None
+    return time.perf_counter() - t0, count[0], x0, kind
+
+
+def call_count(T, warmup, p):
+    """Busiest-device predictor calls: warmup + ceil((T-warmup)/p) (commodel.py:60-68)."""
+    return warmup + -(-(T - warmup) // p)
+
+
+def reference_arm(args, cfg, world, rank):
+    if rank != 0:
+        return
+    import numpy as np  # noqa: F401
+
+    ncores = len(os.sched_getaffinity(0))
+    T, w = cfg["T"], cfg["warmup"] if world > 1 else 0
+    calls = call_count(T, w, world)
+    sample = max(1, min(T, args.ref_sample))
+    times = []
+    kind = "port"
+    for i in range(args.warmup + args.steps):
+        el, done, _, kind = cpu_reference_run(cfg, max_forwards=sample)
+        per_call = el / done
+        if i >= args.warmup:
+            times.append(per_call * calls * 1e3)
+    val = statistics.mean(times)
+    out = {
+        "impl": "reference",
+        "metric": f"denoise latency ({T} steps, degree {world})",
+        "value": val, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": val, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded reference RNG)",
+        "config": config_block(args, cfg, world),
+        "cpu_baseline": {"value": val, "unit": "ms", "cores": ncores, "kind": kind,
+                         "sample": f"first {sample} of {T} sampler steps of the reference's "
+                                   f"sequential loop per step, extrapolated x{calls} predictor "
+                                   f"calls (busiest device at degree {world}, "
+                                   f"commodel.call_count_per_device)"},
+        "e2e": {"value": val, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def config_block(args, cfg, world):
+    from paper_2505_14741_b200.spec import SPECS
+
+    b = {"workload": args.config, "baseline_config_index": cfg["baseline_config"],
+         "steps_T": cfg["T"], "sampler": f"DDPM posterior-mean, sigma_mode={cfg['sigma']} "
+                                          "(the reference's deterministic 'DDIM' mode)",
+         "degree": world, "warmup_steps": cfg["warmup"] if world > 1 else 0,
+         "precision": cfg["precision"], "l2": "flushed (512 MiB write) between timed runs",
+         "parallelism": f"parastep-d{world}" if world > 1 else "sequential (degree 1)"}
+    if cfg["spec"]:
+        s = SPECS[cfg["spec"]]
+        b.update({"predictor": cfg["spec"], "latent": f"{s.channels}x{s.height}x{s.width}"
+                  if s.frames == 1 else f"{s.frames}x{s.height}x{s.width}x{s.channels}",
+                  "hidden": s.hidden, "depth": s.depth, "heads": s.heads, "tokens": s.tokens})
+    else:
+        b.update({"predictor": "reference MLP 4112-64-64-4096", "latent": "4x32x32"})
+    return b
+
+
+# ------------------------------------------------------------------ GPU arm
+def make_sampler(w, sched, rcfg, world, record=False, external_init=False):
+    if world == 1:
+        from paper_2505_14741_b200.engines import DeviceSampler
+
+        return DeviceSampler(w, sched, rcfg, record=record, external_init=external_init)
+    from paper_2505_14741_b200.protocol import NcclSampler
+
+    return NcclSampler(w, sched, rcfg, record=record, external_init=external_init)
+
+
+def launches_of(s):
+    return s.ops.launches if hasattr(s, "ops") else s.launches
+
+
+def time_runs(sampler, K, W, flush, torch, dist, world, seed0=0):
+    for i in range(W):
+        sampler.run(seed0 + i, graph=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    evs = []
+    for i in range(K):
+        flush.zero_()  # untimed: evict L2 between timed runs
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        sampler.run(seed0 + i, graph=True)
+        b.record()
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    ms = [a.elapsed_time(b) for a, b in evs]
+    if world > 1:
+        t = torch.tensor(ms, device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.tolist()
+        dist.barrier()
+    return ms
+
+
+def gemm_roofline(w, cfg, torch, bf16_peak):
+    """Dominant kernel: the tcgen05 GEMM of the MLP fc1 layer (M = tokens)."""
+    if cfg["spec"] is None:
+        return None
+    which = 2
+    M, N, K = w.gemm_shape(which, 1)
+    w.bench_gemm(which, 1, 3)
+    torch.cuda.synchronize()
+    iters = 50
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    w.bench_gemm(which, 1, iters)
+    b.record()
+    torch.cuda.synchronize()
+    t = a.elapsed_time(b) / iters * 1e-3
+    flops = 2.0 * M * N * K
+    if cfg["precision"] == "bf16":
+        peak, note = bf16_peak, "measured bf16 dense (burst)"
+    else:
+        peak = bf16_peak / 2 / 3
+        note = ("3xTF32: measured bf16 dense x 1/2 (tf32 rate) / 3 passes = fp32-accurate "
+                "tensor peak")
+    achieved = flops / t / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(f"{cfg['spec']}_{cfg['precision']}_fc1")
+    return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak, "traffic": traffic,
+            "kernel": f"gemm_tc fc1 M={M} N={N} K={K} ({cfg['precision']})",
+            "launch_us": t * 1e6, "peak_note": note}
+
+
+def sched_roofline(torch, hbm_peak):
+    """The fused apply kernel on an HBM-sized vector (8 apply steps, fp32)."""
+    from paper_2505_14741_b200 import _lib
+    from paper_2505_14741_b200.schedule import make_default_schedule, step_coeffs
+
+    lib = _lib.load()
+    n = 1 << 26
+    c = 8
+    x = torch.randn(n, device="cuda")
+    eps = torch.randn((c, n), device="cuda")
+    seed = torch.zeros(1, dtype=torch.int64, device="cuda")
+    sch = make_default_schedule(50, "zero")
+    steps = _lib.step_array([step_coeffs(sch, t) for t in range(20, 20 - c, -1)])
+    E = _lib.ptr_array([_lib.ptr(eps) + k * n * 4 for k in range(c)])
+    R = _lib.ptr_array([0] * c)
+
+    def go():
+        _lib.check(lib.ps_sched_cycle(_lib.ptr(x), _lib.ptr(x), n, _lib.PS_F32, _lib.ptr(seed), c,
+                                      steps, E, R, 0, 0, _lib.step_array([]), _lib.ptr_array([]),
+                                      _lib.ptr_array([]), _lib.stream_ptr()), "cycle")
+
+    go()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    iters = 10
+    a.record()
+    for _ in range(iters):
+        go()
+    b.record()
+    torch.cuda.synchronize()
+    t = a.elapsed_time(b) / iters * 1e-3
+    bytes_ = (c + 2) * n * 4
+    gbs = bytes_ / t / 1e9
+    return {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
+            "frac": gbs / hbm_peak, "kernel": f"sched_cycle apply c={c} fp32 n=2^26 (zero mode)",
+            "launch_us": t * 1e6}
+
+
+def our_arm(args, cfg, world, rank, local):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_14741_b200.schedule import make_default_schedule
+
+    torch.cuda.set_device(local)
+    hbm_peak, bf16_peak, peak_src = measured_peaks()
+    w = build_predictor(cfg, max_batch=8)
+    n = w.data_dim
+    sched = make_default_schedule(cfg["T"], cfg["sigma"])
+    rcfg = run_cfg(cfg, n, world)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+
+    sampler = make_sampler(w, sched, rcfg, world)
+    clocks = ClockSampler(local)
+    sampler.run(0, graph=True)  # capture
+    torch.cuda.synchronize()
+    with clocks:
+        ms = time_runs(sampler, args.steps, args.warmup, flush, torch, dist, world)
+    launches = launches_of(sampler)
+    value = statistics.mean(ms)
+
+    # e2e through the public API: host x_T in (pinned), full Trajectory out
+    es = 8 if w.state_dtype_code == 0 else 4
+    x_host = torch.from_numpy(np.random.default_rng(1).standard_normal(n)).to(
+        torch.float64 if es == 8 else torch.float32).pin_memory()
+    e2s = make_sampler(w, sched, rcfg, world, record=True, external_init=True)
+    e2e_ms = []
+    for i in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        e2s.run(i, graph=True, x_init=x_host)
+        if world == 1:
+            tr = e2s.trajectory()
+            assert tr.steps == cfg["T"]
+        else:
+            res = e2s.result()
+            assert res.x0.shape[0] == n
+        dt = (time.perf_counter() - t0) * 1e3
+        if i >= args.warmup:
+            e2e_ms.append(dt)
+    if world > 1:
+        t = torch.tensor(e2e_ms, device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = t.tolist()
+    e2e = statistics.mean(e2e_ms)
+    d2h = ((2 * cfg["T"] + 1) * n * es) if rank == 0 else n * es
+
+    roof = gemm_roofline(w, cfg, torch, bf16_peak) if rank == 0 else None
+    roof_sched = sched_roofline(torch, hbm_peak) if rank == 0 else None
+
+    extra = {}
+    cpu = None
+    rel = None
+    if rank == 0 and world == 1:
+        # single-GPU BatchStep (lanes batched into one forward): the paper's s=2/4/8
+        for d in args.batchstep:
+            bs = make_sampler(w, sched, run_cfg(cfg, n, d, "batchstep"), 1)
+            bs.run(0, graph=True)
+            bms = time_runs(bs, max(2, args.steps // 2), 1, flush, torch, dist, 1)
+            extra[f"batchstep_d{d}_ms"] = statistics.mean(bms)
+            extra[f"batchstep_d{d}_speedup"] = value / statistics.mean(bms)
+        if not args.no_cpu_baseline:
+            # the reference sampler on host cores; one full denoise when it fits
+            ncores = len(os.sched_getaffinity(0))
+            full = cfg["spec"] in (None, "dit_s2")
+            el, done, x0_ref, kind = cpu_reference_run(
+                cfg, max_forwards=None if full else args.ref_sample)
+            ref_ms = el / done * cfg["T"] * 1e3
+            cpu = {"value": ref_ms, "unit": "ms", "cores": ncores, "kind": kind,
+                   "sample": (f"one full {cfg['T']}-step sequential denoise (seed 0)" if full else
+                              f"first {done} of {cfg['T']} steps, extrapolated x{cfg['T']}")}
+            if x0_ref is not None:
+                seq = make_sampler(w, sched, run_cfg(cfg, n, 1), 1, record=False)
+                seq.run(0)
+                torch.cuda.synchronize()
+                from paper_2505_14741_b200.numerics import rel_mae
+
+                rel = rel_mae(x0_ref, seq.x0_device.double().cpu().numpy())
+    if rank != 0:
+        return
+    out = {
+        "metric": f"denoise latency ({cfg['T']} steps, degree {world})",
+        "value": value, "unit": "ms", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": {"fp32": "f32", "bf16": "bf16", "fp64": "f64"}[cfg["precision"]],
+        "data": "synthetic: seeded reference-RNG latent, random-init weights (Xavier, ref. "
+                "convention)",
+        "config": config_block(args, cfg, world),
+        "clocks": clocks.summary(),
+        "e2e": {"value": e2e, "unit": "ms", "h2d_bytes_per_step": n * es,
+                "d2h_bytes_per_step": d2h,
+                "api": "DeviceSampler.sample path: x_T from pinned host, Trajectory to numpy"},
+        "gpu_launches": launches * args.steps,
+        "launches_per_denoise": launches,
+        "roofline": roof,
+        "roofline_sched": roof_sched,
+        "peaks_source": peak_src,
+        "cpu_baseline": cpu,
+        "rel_mae_vs_reference": rel,
+        "samples_ms": ms,
+    }
+    out.update(extra)
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="small_dit_fp32", choices=sorted(CONFIGS))
+    ap.add_argument("--batchstep", type=int, nargs="*", default=[2, 4, 8])
+    ap.add_argument("--ref-sample", type=int, default=3,
+                    help="reference arm: sampler steps timed per bench step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_setup()
+    if world != args.gpus:
+        log(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}; using WORLD_SIZE")
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        reference_arm(args, cfg, world, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    try:
+        our_arm(args, cfg, world, rank, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

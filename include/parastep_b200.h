@@ -144,6 +144,13 @@ int ps_dit_destroy(ps_dit* h);
 /* algorithmic FLOPs of one forward of one sample (GEMMs + attention) */
 double ps_dit_flops(const ps_dit* h);
 
+/* number of kernel launches one ps_dit_forward issues */
+int ps_dit_kernels_per_forward(const ps_dit* h);
+/* Roofline probe: launch block 0's GEMM `which` (0 qkv, 1 proj, 2 fc1,
+ * 3 fc2) `iters` times back to back on the stream with M = B x tokens rows
+ * (plain store epilogue into handle scratch). */
+int ps_dit_bench_gemm(ps_dit* h, int which, int B, int iters, void* cuda_stream);
+
 /* Diagnostic (allocates + synchronises; never on the hot path):
  * C[M,N] = A[M,K] W[K,N] + bias with fp32 buffers in the reference layout,
  * through the tcgen05 kernel (impl 2; precision 1 = bf16, 0 = 3xTF32) or the

@@ -72,6 +72,8 @@ _SIGS = {
                                  C.c_void_p, C.c_void_p]),
     "ps_dit_destroy": (C.c_int, [C.c_void_p]),
     "ps_dit_flops": (C.c_double, [C.c_void_p]),
+    "ps_dit_kernels_per_forward": (C.c_int, [C.c_void_p]),
+    "ps_dit_bench_gemm": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]),
     "ps_gemm_test": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
                                C.c_int, C.c_int, C.c_int, C.c_void_p]),
 }

@@ -203,6 +203,7 @@ int ps_dit_create(const ps_dit_config* cfg, const ps_dit_weights* w, ps_dit** ou
       return rc;
     }
   }
+  cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     ps_dit_destroy(h);
@@ -216,6 +217,29 @@ int ps_dit_create(const ps_dit_config* cfg, const ps_dit_weights* w, ps_dit** ou
 }
 
 double ps_dit_flops(const ps_dit* h) { return h ? h->flops : 0.0; }
+
+int ps_dit_kernels_per_forward(const ps_dit* h) {
+  // 3 conditioning GEMVs + patch embed + 7 per block + final LN + final GEMM
+  return h ? 3 + 1 + 7 * h->depth + 2 : 0;
+}
+
+int ps_dit_bench_gemm(ps_dit* h, int which, int B, int iters, void* cs) {
+  PS_CHECK_ARG(h && which >= 0 && which < 4 && B >= 1 && B <= h->cfg.max_batch && iters >= 1,
+               "bad bench_gemm arguments");
+  const int D = h->D, M = B * h->L;
+  const int Ns[4] = {3 * D, D, h->Dm, D}, Ks[4] = {D, D, D, h->Dm};
+  const float* Ws[4] = {h->blk[0].qkv, h->blk[0].proj, h->blk[0].fc1, h->blk[0].fc2};
+  const TcOperand* A = h->use_tc ? (which == 3 ? &h->tca.hid : &h->tca.a) : nullptr;
+  Epi e{};
+  e.mode = EPI_STORE;
+  e.out = Ns[which] > 3 * D ? h->hid : h->qkv;  // scratch: qkv is M x 3D, hid is M x Dm
+  for (int i = 0; i < iters; ++i) {
+    int rc = gemm(h, which, which == 3 ? h->hid : h->a, A, Ws[which], M, Ns[which], Ks[which], e,
+                  as_stream(cs));
+    if (rc) return rc;
+  }
+  return 0;
+}
 
 int ps_dit_destroy(ps_dit* h) {
   if (!h) return 0;
@@ -263,11 +287,6 @@ int ps_dit_forward(ps_dit* h, const float* x, const int32_t* host_ts, int B, flo
     at.out_f32 = h->o;
   }
   const size_t at_smem = (size_t)(AT_K * (h->dh + 1) + AT_K * h->dh + AT_Q * h->dh) * sizeof(float);
-  static bool at_attr = false;
-  if (!at_attr) {
-    cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    at_attr = true;
-  }
   for (int i = 0; i < h->depth; ++i) {
     const BlockW& bw = h->blk[i];
     const int base = i * 6 * D;

@@ -130,6 +130,19 @@ class DiTWeights:
     def flops_per_forward(self) -> float:
         return float(self._lib.ps_dit_flops(self._h))
 
+    def kernels_per_forward(self, B: int = 1) -> int:
+        return int(self._lib.ps_dit_kernels_per_forward(self._h))
+
+    def bench_gemm(self, which: int, B: int, iters: int, stream=None) -> None:
+        """Launch block 0's GEMM `which` (0 qkv, 1 proj, 2 fc1, 3 fc2) iters times (async)."""
+        _lib.check(self._lib.ps_dit_bench_gemm(self._h, which, B, iters, _lib.stream_ptr(stream)),
+                   "bench_gemm")
+
+    def gemm_shape(self, which: int, B: int = 1) -> tuple[int, int, int]:
+        s = self.spec
+        D, M = s.hidden, B * s.tokens
+        return [(M, 3 * D, D), (M, D, D), (M, s.mlp_hidden, D), (M, D, s.mlp_hidden)][which]
+
     def forward_device(self, x, ts, T: int, out, stream=None) -> None:
         """x, out: CUDA float32 [B, data_dim]; ts: B step indices (<= 1000). Async."""
         B = len(ts)

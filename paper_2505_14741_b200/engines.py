@@ -214,7 +214,7 @@ class DeviceSampler:
     """
 
     def __init__(self, w, sched: NoiseSchedule, cfg: RunConfig, record: bool = True,
-                 batched: bool | None = None):
+                 batched: bool | None = None, external_init: bool = False):
         import torch
 
         _check(w, sched, cfg, None)
@@ -246,6 +246,8 @@ class DeviceSampler:
         self.batch_calls = 0
         self.forward_calls = 0
         self.graph = None
+        self.external_init = external_init
+        self.launches = 0  # kernels issued by one run (counted at issue time)
         self._steps = {t: step_coeffs(sched, t) for t in range(1, self.T + 1)}
 
     # ------------------------------------------------------------ launches
@@ -274,14 +276,19 @@ class DeviceSampler:
             x0, x0, self.n, self.dtype_code, _lib.ptr(self.seed_buf), na, A, E, R,
             lane_lo, lane_hi, roll, _lib.ptr_array(caches), _lib.ptr_array(outs), st),
             "sched_cycle")
+        self.launches += 1
 
     def _forward(self, lane_lo: int, lane_hi: int, ts: list[int], row0: int):
         x = self.lanes[lane_lo:lane_hi]
         out = self.eps[row0:row0 + (lane_hi - lane_lo)]
         self.w.forward_device(x, ts, self.T, out)
         self.forward_calls += 1
+        self.launches += self.w.kernels_per_forward(len(ts))
 
     def _init_x(self):
+        if self.external_init:
+            return  # x_T was copied into lanes[0] by run(x_init=...)
+        self.launches += 1
         _lib.check(self.lib.ps_rng_normal_dev(
             self._row(self.lanes, 0), self.n, _lib.ptr(self.seed_buf),
             stream_id(PURPOSE_INIT, 0), 0, self.dtype_code, _lib.stream_ptr()), "initial_state")
@@ -289,6 +296,7 @@ class DeviceSampler:
     def _launch(self):
         cfg = self.cfg
         self.forward_calls = 0
+        self.launches = 0
         self._init_x()
         T = self.T
         if cfg.strategy == STRATEGY_SEQUENTIAL:
@@ -350,11 +358,20 @@ class DeviceSampler:
                 self._cycle(list(cyc), [k0 + j for j in range(c)])
         self.batch_calls = nb if self.batched else 0
 
-    def run(self, seed: int, graph: bool = False) -> None:
-        """Issue one full denoise for `seed` on the current stream (async)."""
+    def run(self, seed: int, graph: bool = False, x_init=None) -> None:
+        """Issue one full denoise for `seed` on the current stream (async).
+
+        With ``external_init`` the caller provides x_T (``x_init``: a host
+        tensor, ideally pinned, or a device tensor) instead of the in-kernel
+        draw; it is copied into the state buffer on the stream first.
+        """
         import torch
 
         self.seed_buf.fill_(_int64_of(seed))
+        if self.external_init:
+            if x_init is None:
+                raise ConfigError("external_init sampler needs x_init")
+            self.lanes[0].copy_(torch.as_tensor(x_init).reshape(-1), non_blocking=True)
         if not graph:
             self._launch()
             return
@@ -374,6 +391,11 @@ class DeviceSampler:
     @property
     def x0_device(self):
         return self.lanes[0]
+
+    def sample(self, seed: int, x_init=None, graph: bool = True) -> Trajectory:
+        """Public one-call API: (optional host x_T) -> full Trajectory on host."""
+        self.run(seed, graph=graph, x_init=x_init)
+        return self.trajectory()
 
     def trajectory(self) -> Trajectory:
         """Copy the run's records to host (reference Trajectory of float64 vectors)."""

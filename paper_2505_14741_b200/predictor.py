@@ -140,6 +140,9 @@ class PredictorWeights:
         dev["desc"].temb_table = _lib.ptr(dev["temb"][T])
         return dev
 
+    def kernels_per_forward(self, B: int = 1) -> int:
+        return 2 * len(self.layers)  # split-K partial + finish per layer
+
     def forward_device(self, x, ts, T: int, out, stream=None) -> None:
         """x, out: CUDA float64 [B, data_dim]; ts: B step indices. Async."""
         lib = _lib.load()

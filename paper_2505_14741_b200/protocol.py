@@ -1,0 +1,275 @@
+"""Multi-GPU ParaStep: one process per GPU, one eps all-gather per round.
+
+Replaces the reference's distributed worker (pkg/src/parastep/protocol/
+worker.py:149-241: NOISE master->rank 0, SAMPLE_BCAST rank 0->all) with the
+cycle form the reference's own tests pin to it (tests/test_engines.py:294-303,
+test_protocol.py:44-55):
+
+    warm-up   every rank runs the same steps redundantly (worker.py:180-185);
+              the kernels are deterministic, so every rank holds the same bits
+    cycle     rank r owns lane r: x_r = roll^r(x_sync, own cache)   (fused)
+              eps_r = forward(x_r, t_r)
+              E = all_gather(eps_0..eps_{p-1})          (NCCL over NVLink)
+              x_sync = step^c(x_sync, E)  on EVERY rank  (fused apply, which
+              also rolls the rank's lane for the next cycle)
+
+The redundant deterministic apply replaces the gather-to-0 + broadcast, so
+each rank sends N*s bytes and receives (p-1)*N*s per cycle. A truncated last
+cycle (c < p) idles ranks >= c (worker.py module docstring).
+
+``rank_loop`` holds the protocol logic once; it is driven by ``CudaRankOps``
+(the product: C-ABI kernels + NCCL via torch.distributed) and, in the CPU
+tests, by an oracle-backed ops object over gloo (tests/test_protocol_gloo.py).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from . import _lib
+from .engines import (
+    STRATEGY_PARASTEP,
+    RunConfig,
+    StepRecord,
+    Trajectory,
+    _check,
+    _int64_of,
+    plan_cycles,
+)
+from .errors import ConfigError, ProtocolAbortError
+from .numerics import PURPOSE_INIT, stream_id
+from .schedule import NoiseSchedule, step_coeffs
+
+
+def rank_loop(ops, T: int, warmup: int, p: int, rank: int, cycles: list[list[int]]):
+    """One rank's ParaStep run over abstract ops; returns the final x handle.
+
+    ops.init() -> x; ops.forward(x, t, slot) -> eps; ops.zeros(slot) -> eps;
+    ops.allgather(eps) -> list of p eps; ops.apply_roll(x, apply_ts, eps_list,
+    roll_ts, cache) -> (x, lane_x) with roll_ts == [] meaning no roll.
+    ops.record(k, eps) optionally stores trajectory eps rows.
+    """
+    x = ops.init()
+    lane_x = None
+    cache = None
+    warm_ts = list(range(T, T - warmup, -1))
+    for i, t in enumerate(warm_ts):
+        e = ops.forward(x, t, "warm")
+        ops.record(T - t, [e])
+        nxt = cycles[0] if (i == len(warm_ts) - 1 and cycles) else None
+        roll = nxt[:rank] if (nxt is not None and 1 <= rank < len(nxt)) else []
+        cache = e
+        x, lane_x = ops.apply_roll(x, [t], [e], roll, cache)
+    for ci, cyc in enumerate(cycles):
+        c = len(cyc)
+        mine = rank < c
+        if mine:
+            e_local = ops.forward(x if rank == 0 else lane_x, cyc[rank], "lane")
+        else:
+            e_local = ops.zeros("lane")
+        gathered = ops.allgather(e_local)
+        ops.record(T - cyc[0], gathered[:c])
+        if mine:
+            cache = ops.keep_cache(gathered[rank])
+        nxt = cycles[ci + 1] if ci + 1 < len(cycles) else None
+        roll = nxt[:rank] if (nxt is not None and 1 <= rank < len(nxt)) else []
+        x, lane_x = ops.apply_roll(x, list(cyc), gathered[:c], roll, cache)
+    return x
+
+
+class CudaRankOps:
+    """Device buffers + C-ABI launches + NCCL all-gather for one rank."""
+
+    def __init__(self, w, sched: NoiseSchedule, cfg: RunConfig, rank: int, world: int,
+                 group=None, record: bool = False, external_init: bool = False):
+        import torch
+
+        self.torch = torch
+        self.lib = _lib.load(require_gpu=True)
+        self.w, self.sched, self.cfg = w, sched, cfg
+        self.rank, self.world, self.group = rank, world, group
+        self.n, self.T = cfg.data_dim, cfg.steps
+        self.code = w.state_dtype_code
+        tdt = torch.float64 if self.code == _lib.PS_F64 else torch.float32
+        n = self.n
+        self.seed_buf = torch.zeros(1, dtype=torch.int64, device="cuda")
+        self.x = torch.zeros(n, dtype=tdt, device="cuda")
+        self.lane = torch.zeros(n, dtype=tdt, device="cuda")
+        self.e_warm = torch.zeros(n, dtype=tdt, device="cuda")
+        self.e_local = torch.zeros(n, dtype=tdt, device="cuda")
+        self.gathered = torch.zeros((world, n), dtype=tdt, device="cuda")
+        self.cache_buf = torch.zeros(n, dtype=tdt, device="cuda")
+        self.record_on = record
+        self.rec_x = torch.zeros((self.T, n), dtype=tdt, device="cuda") if record else None
+        self.rec_e = torch.zeros((self.T, n), dtype=tdt, device="cuda") if record else None
+        self.external_init = external_init
+        self._steps = {t: step_coeffs(sched, t) for t in range(1, self.T + 1)}
+        cyc = plan_cycles(cfg)
+        # lane caches must outlive a cycle only if some cycle is longer than its predecessor
+        self.persist_cache = any(len(b) > len(a) for a, b in zip(cyc, cyc[1:]))
+        self.launches = 0
+        self.gathers = 0
+
+    def _p(self, t) -> int:
+        return _lib.ptr(t)
+
+    def init(self):
+        if not self.external_init:
+            _lib.check(self.lib.ps_rng_normal_dev(
+                self._p(self.x), self.n, self._p(self.seed_buf), stream_id(PURPOSE_INIT, 0), 0,
+                self.code, _lib.stream_ptr()), "initial_state")
+            self.launches += 1
+        return self.x
+
+    def forward(self, x, t, slot):
+        out = self.e_warm if slot == "warm" else self.e_local
+        self.w.forward_device(x.view(1, -1), [t], self.T, out.view(1, -1))
+        self.launches += self.w.kernels_per_forward(1)
+        return out
+
+    def zeros(self, slot):
+        return self.e_local  # idle rank: contents ignored by every receiver
+
+    def allgather(self, e):
+        import torch.distributed as dist
+
+        dist.all_gather_into_tensor(self.gathered, e, group=self.group)
+        self.gathers += 1
+        return [self.gathered[i] for i in range(self.world)]
+
+    def keep_cache(self, e):
+        if self.persist_cache:
+            self.cache_buf.copy_(e)
+            return self.cache_buf
+        return e
+
+    def record(self, k, eps_list):
+        if self.record_on:
+            self.rec_e[k:k + len(eps_list)].copy_(self.torch.stack(eps_list))
+
+    def apply_roll(self, x, apply_ts, eps_list, roll_ts, cache):
+        es = x.element_size()
+        A = _lib.step_array([self._steps[t] for t in apply_ts])
+        E = _lib.ptr_array([self._p(e) for e in eps_list])
+        R = _lib.ptr_array([(self._p(self.rec_x) + (self.T - t) * self.n * es)
+                            if self.record_on else 0 for t in apply_ts])
+        lane_hi = self.rank + 1 if roll_ts else 0
+        caches = [0] * _lib.PS_MAX_CYCLE
+        outs = [0] * _lib.PS_MAX_CYCLE
+        roll = _lib.step_array([self._steps[t] for t in roll_ts])
+        if roll_ts:
+            caches[self.rank] = self._p(cache)
+            outs[self.rank] = self._p(self.lane)
+        _lib.check(self.lib.ps_sched_cycle(
+            self._p(x), self._p(x), self.n, self.code, self._p(self.seed_buf), len(apply_ts), A, E,
+            R, self.rank if roll_ts else 0, lane_hi, roll, _lib.ptr_array(caches),
+            _lib.ptr_array(outs), _lib.stream_ptr()), "sched_cycle")
+        self.launches += 1
+        return x, self.lane
+
+
+@dataclass
+class RunResult:
+    """Per-rank outcome of run_nccl (mirrors worker.RunResult, worker.py:97-110)."""
+
+    trajectory: Trajectory | None
+    x0: object
+    rank: int
+    world: int
+    gathers: int = 0
+    launches: int = 0
+    timings: dict = field(default_factory=dict)
+
+
+class NcclSampler:
+    """ParaStep over `world` GPUs (degree == world), replayable per seed.
+
+    Must be constructed on every rank of an initialised NCCL process group;
+    ``run(seed)`` issues the run on the current stream (async). With
+    ``graph=True`` the whole run, NCCL all-gathers included, is captured in
+    one CUDA graph after an eager warm-up run.
+    """
+
+    def __init__(self, w, sched: NoiseSchedule, cfg: RunConfig, group=None, record=False,
+                 external_init=False):
+        import torch.distributed as dist
+
+        _check(w, sched, cfg, STRATEGY_PARASTEP)
+        if not dist.is_initialized():
+            raise ConfigError("run_nccl needs an initialised torch.distributed process group")
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        if cfg.degree != self.world:
+            raise ConfigError(f"degree {cfg.degree} != world size {self.world}")
+        self.cfg = cfg
+        self.cycles = plan_cycles(cfg)
+        self.ops = CudaRankOps(w, sched, cfg, self.rank, self.world, group, record, external_init)
+        self.graph = None
+
+    def _launch(self):
+        self.ops.launches = 0
+        self.ops.gathers = 0
+        rank_loop(self.ops, self.cfg.steps, self.cfg.warmup, self.world, self.rank, self.cycles)
+
+    def run(self, seed: int, graph: bool = False, x_init=None) -> None:
+        import torch
+
+        self.ops.seed_buf.fill_(_int64_of(seed))
+        if self.ops.external_init:
+            if x_init is None:
+                raise ConfigError("external_init sampler needs x_init")
+            self.ops.x.copy_(torch.as_tensor(x_init).reshape(-1), non_blocking=True)
+        if not graph:
+            self._launch()
+            return
+        if self.graph is None:
+            self._launch()
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(g, stream=s):
+                    self._launch()
+            torch.cuda.current_stream().wait_stream(s)
+            self.graph = g
+        self.graph.replay()
+
+    def result(self) -> RunResult:
+        import torch
+
+        torch.cuda.current_stream().synchronize()
+        o = self.ops
+        traj = None
+        if o.record_on and self.rank == 0:
+            xs = o.rec_x.double().cpu().numpy()
+            es = o.rec_e.double().cpu().numpy()
+            T = self.cfg.steps
+            fresh = [True] * T
+            for cyc in self.cycles:
+                for j, t in enumerate(cyc):
+                    fresh[T - t] = j == 0
+            traj = Trajectory([StepRecord(T - k, xs[k].copy(), es[k].copy(), fresh[k])
+                               for k in range(T)], o.x.double().cpu().numpy().copy())
+        return RunResult(traj, o.x.double().cpu().numpy().copy(), self.rank, self.world,
+                         o.gathers, o.launches)
+
+
+def run_nccl(w, sched: NoiseSchedule, cfg: RunConfig, group=None, record: bool = True,
+             timeout: float = 60.0) -> RunResult:
+    """The reference's run_tcp/run_loopback (worker.py:244-372) as one NCCL rank.
+
+    Call on every rank of an initialised NCCL group with cfg.degree == world
+    size. Rank 0's result carries the Trajectory; every rank returns its x0
+    (identical on all ranks). A failed collective surfaces as
+    ProtocolAbortError(rank, step) like the reference's transport faults.
+    """
+    import torch
+
+    s = NcclSampler(w, sched, cfg, group=group, record=record)
+    try:
+        s.run(cfg.seed)
+        torch.cuda.synchronize()
+    except RuntimeError as exc:  # NCCL / CUDA failure during the round
+        raise ProtocolAbortError(f"collective failed: {exc}", s.rank) from exc
+    return s.result()

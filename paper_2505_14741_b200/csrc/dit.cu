@@ -12,6 +12,11 @@
 
 using namespace ps;
 
+static __global__ void f32_to_bf16_kernel(const float* in, __nv_bfloat16* out, size_t n) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = __float2bfloat16_rn(in[i]);
+}
+
 struct BlockW {
   const float *ada, *qkv, *proj, *fc1, *fc2;
   const float *b_ada, *b_qkv, *b_proj, *b_fc1, *b_fc2;
@@ -29,6 +34,7 @@ struct ps_dit {
   // owned device memory
   std::vector<void*> owned;
   float *Wada_all, *bada_all;
+  __nv_bfloat16* Wada_bf16;  // bf16 copy for the bf16 precision path
   float *h, *a, *qkv, *o, *hid, *t1, *silu_c, *mod;
   // tensor-core operand copies (gemm_tc.cuh)
   TcWeights tcw;
@@ -49,7 +55,23 @@ static int dalloc_t(ps_dit* h, T** p, size_t count) {
   return dalloc(h, reinterpret_cast<void**>(p), count * sizeof(T) + 256);
 }
 
-static int gemv(const float* in, int64_t in_stride, const int32_t* rows, const float* W,
+template <typename TW, int MAXB>
+static void gemv_launch(const GemvArgs& p, cudaStream_t st) {
+  constexpr int C = GvLoad<TW>::C;
+  const size_t smem = gemv_smem<TW>(p.B, p.K);
+  gemv_kernel<TW, MAXB><<<(p.N + 32 * C - 1) / (32 * C), GV_WARPS * 32, smem, st>>>(p);
+}
+
+template <typename TW>
+static void gemv_set_attr() {
+  cudaFuncSetAttribute(gemv_kernel<TW, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
+  cudaFuncSetAttribute(gemv_kernel<TW, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
+  cudaFuncSetAttribute(gemv_kernel<TW, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
+  cudaFuncSetAttribute(gemv_kernel<TW, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
+}
+
+// W is fp32 or bf16 (wbf16), (K, N) row-major, N % (4|8) == 0
+static int gemv(const float* in, int64_t in_stride, const int32_t* rows, const void* W, bool wbf16,
                 const float* bias, float* out, int K, int N, int B, int act, cudaStream_t st) {
   GemvArgs p{};
   p.in = in;
@@ -62,7 +84,17 @@ static int gemv(const float* in, int64_t in_stride, const int32_t* rows, const f
   p.N = N;
   p.B = B;
   p.act = act;
-  gemv_kernel<<<(N + GV_COLS - 1) / GV_COLS, GV_COLS * GV_KGRP, 0, st>>>(p);
+  if (wbf16) {
+    if (B <= 1) gemv_launch<__nv_bfloat16, 1>(p, st);
+    else if (B <= 4) gemv_launch<__nv_bfloat16, 4>(p, st);
+    else if (B <= 8) gemv_launch<__nv_bfloat16, 8>(p, st);
+    else gemv_launch<__nv_bfloat16, 16>(p, st);
+  } else {
+    if (B <= 1) gemv_launch<float, 1>(p, st);
+    else if (B <= 4) gemv_launch<float, 4>(p, st);
+    else if (B <= 8) gemv_launch<float, 8>(p, st);
+    else gemv_launch<float, 16>(p, st);
+  }
   return check_launch("gemv");
 }
 
@@ -85,7 +117,7 @@ static int ln_mod(ps_dit* h, int rows, int shift_off, int scale_off, const TcOpe
   } else {
     p.out_f32 = h->a;
   }
-  const int threads = 256;
+  const int threads = 256;  // 8 rows per block
   ln_mod_kernel<<<(rows * 32 + threads - 1) / threads, threads, 0, st>>>(p);
   return check_launch("ln_mod");
 }
@@ -108,6 +140,8 @@ int ps_dit_create(const ps_dit_config* cfg, const ps_dit_weights* w, ps_dit** ou
   const int D = cfg->hidden, depth = cfg->depth;
   PS_CHECK_ARG(D % cfg->heads == 0, "hidden % heads != 0");
   PS_CHECK_ARG(D / cfg->heads <= 32 * AT_MAXU, "head_dim > 128 unsupported");
+  PS_CHECK_ARG((D / cfg->heads) % 4 == 0, "head_dim must be a multiple of 4");
+  PS_CHECK_ARG(D % 8 == 0 && D <= 2048, "hidden must be a multiple of 8 and <= 2048");
   PS_CHECK_ARG(cfg->max_batch >= 1 && cfg->max_batch <= GV_MAXB, "max_batch must be in [1, 16]");
   PS_CHECK_ARG(w->n_layers == 3 + 5 * depth + 2, "weight count does not match depth");
   ps_dit* h = new ps_dit();
@@ -180,8 +214,16 @@ int ps_dit_create(const ps_dit_config* cfg, const ps_dit_weights* w, ps_dit** ou
       return fail((int)e, std::string("ada concat: ") + cudaGetErrorString(e));
     }
   }
+  if (cfg->precision == 1) {
+    const size_t na = (size_t)D * h->n_ada;
+    if ((rc = dalloc_t(h, &h->Wada_bf16, na))) {
+      ps_dit_destroy(h);
+      return rc;
+    }
+    f32_to_bf16_kernel<<<(unsigned)((na + 255) / 256), 256>>>(h->Wada_all, h->Wada_bf16, na);
+  }
   const int impl = cfg->gemm_impl;
-  h->use_tc = (impl == 2) || (impl == 0 && cfg->precision == 1);
+  h->use_tc = (impl == 2) || (impl == 0);  // auto: tcgen05 for both precisions
   if (cfg->precision == 1 && !h->use_tc) {
     ps_dit_destroy(h);
     return fail(PS_EUNSUP, "bf16 precision needs the tensor-core GEMM");
@@ -204,6 +246,9 @@ int ps_dit_create(const ps_dit_config* cfg, const ps_dit_weights* w, ps_dit** ou
     }
   }
   cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(attn_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  gemv_set_attr<float>();
+  gemv_set_attr<__nv_bfloat16>();
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     ps_dit_destroy(h);
@@ -259,10 +304,13 @@ int ps_dit_forward(ps_dit* h, const float* x, const int32_t* host_ts, int B, flo
   const int D = h->D, L = h->L, M = B * L;
   int rc;
   // conditioning: c = temb2(silu(temb1(freq[t]))), all adaLN vectors at once
-  if ((rc = gemv(h->freq, h->freq_dim, host_ts, h->Wt1, h->bt1, h->t1, h->freq_dim, D, B, 1, st)))
+  if ((rc = gemv(h->freq, h->freq_dim, host_ts, h->Wt1, false, h->bt1, h->t1, h->freq_dim, D, B, 1,
+                 st)))
     return rc;
-  if ((rc = gemv(h->t1, D, nullptr, h->Wt2, h->bt2, h->silu_c, D, D, B, 1, st))) return rc;
-  if ((rc = gemv(h->silu_c, D, nullptr, h->Wada_all, h->bada_all, h->mod, D, h->n_ada, B, 0, st)))
+  if ((rc = gemv(h->t1, D, nullptr, h->Wt2, false, h->bt2, h->silu_c, D, D, B, 1, st))) return rc;
+  const bool abf = h->Wada_bf16 != nullptr;
+  if ((rc = gemv(h->silu_c, D, nullptr, abf ? (const void*)h->Wada_bf16 : (const void*)h->Wada_all,
+                 abf, h->bada_all, h->mod, D, h->n_ada, B, 0, st)))
     return rc;
   patch_embed_kernel<<<M, 128, h->P * sizeof(float), st>>>(x, h->n_latent, h->g, h->P, h->Wpe,
                                                            h->bpe, h->pos, h->h, B);
@@ -287,6 +335,8 @@ int ps_dit_forward(ps_dit* h, const float* x, const int32_t* host_ts, int B, flo
     at.out_f32 = h->o;
   }
   const size_t at_smem = (size_t)(AT_K * (h->dh + 1) + AT_K * h->dh + AT_Q * h->dh) * sizeof(float);
+  const size_t as_smem = attn_small_smem(L, h->dh);
+  const bool small_attn = L <= AS_MAXL && as_smem <= 220 * 1024;
   for (int i = 0; i < h->depth; ++i) {
     const BlockW& bw = h->blk[i];
     const int base = i * 6 * D;
@@ -296,8 +346,13 @@ int ps_dit_forward(ps_dit* h, const float* x, const int32_t* host_ts, int B, flo
     e.bias = bw.b_qkv;
     e.out = h->qkv;
     if ((rc = gemm(h, 4 * i + 0, h->a, aop, bw.qkv, M, 3 * D, D, e, st))) return rc;
-    dim3 ag((L + AT_Q - 1) / AT_Q, h->H, B);
-    attn_kernel<<<ag, AT_WARPS * 32, at_smem, st>>>(at);
+    if (small_attn) {
+      dim3 ag((L + AS_Q - 1) / AS_Q, h->H, B);
+      attn_small_kernel<<<ag, AS_WARPS * 32, as_smem, st>>>(at);
+    } else {
+      dim3 ag((L + AT_Q - 1) / AT_Q, h->H, B);
+      attn_kernel<<<ag, AT_WARPS * 32, at_smem, st>>>(at);
+    }
     if ((rc = check_launch("attn"))) return rc;
     e = Epi{};
     e.mode = EPI_RESID;

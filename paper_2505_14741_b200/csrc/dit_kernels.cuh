@@ -33,50 +33,99 @@ __device__ __forceinline__ float gelu_tanh_f(float v) {
 }
 
 // ---------------------------------------------------------------- GEMV
-// out[b, o] = act(sum_i in_b[i] W[i, o] + bias[o]); W (K, N) row-major.
-// in_b = in + in_row[b] * in_stride (row index per lane, e.g. the step t for
-// the frequency table). 32 columns x 8 k-groups per block, fixed-order
-// smem reduction (deterministic).
-constexpr int GV_COLS = 32, GV_KGRP = 8, GV_MAXB = 16;
+// out[b, o] = act(sum_i in_b[i] W[i, o] + bias[o]); W (K, N) row-major, fp32
+// or bf16. in_b = in + in_row[b] * in_stride (e.g. the step t selects a row
+// of the frequency table). HBM-bound on W: each lane streams 16 B of a row
+// (4 fp32 / 8 bf16 columns), 8 warps split K, the B inputs are staged in
+// smem, and the 8 partial sums are reduced in a fixed order (deterministic).
+constexpr int GV_WARPS = 8, GV_MAXB = 16;
 
 struct GemvArgs {
   const float* in;
   int64_t in_stride;
   int32_t in_row[GV_MAXB];
-  const float* W;
+  const void* W;
   const float* bias;
   float* out;
   int K, N, B, act;  // act: 0 none, 1 silu
 };
 
-static __global__ void __launch_bounds__(GV_COLS * GV_KGRP) gemv_kernel(const __grid_constant__ GemvArgs p) {
-  __shared__ float red[GV_KGRP][GV_MAXB][GV_COLS + 1];
-  const int tx = threadIdx.x % GV_COLS, ty = threadIdx.x / GV_COLS;
-  const int o = blockIdx.x * GV_COLS + tx;
-  float acc[GV_MAXB];
+template <typename TW> struct GvLoad;
+template <> struct GvLoad<float> {
+  static constexpr int C = 4;
+  static __device__ __forceinline__ void ld(const void* W, int64_t idx, float* w) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(W) + idx));
+    w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+  }
+};
+template <> struct GvLoad<__nv_bfloat16> {
+  static constexpr int C = 8;
+  static __device__ __forceinline__ void ld(const void* W, int64_t idx, float* w) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(
+        reinterpret_cast<const __nv_bfloat16*>(W) + idx));
+    const uint32_t u[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-  for (int b = 0; b < GV_MAXB; ++b) acc[b] = 0.f;
-  if (o < p.N) {
-    for (int i = ty; i < p.K; i += GV_KGRP) {
-      const float w = __ldg(p.W + (int64_t)i * p.N + o);
+    for (int q = 0; q < 4; ++q) {
+      w[2 * q] = __uint_as_float(u[q] << 16);
+      w[2 * q + 1] = __uint_as_float(u[q] & 0xFFFF0000u);
+    }
+  }
+};
+
+template <typename TW, int MAXB>
+__global__ void __launch_bounds__(GV_WARPS * 32) gemv_kernel(const __grid_constant__ GemvArgs p) {
+  constexpr int C = GvLoad<TW>::C;
+  extern __shared__ float gv_smem[];
+  float* xin = gv_smem;                          // [B][K]
+  float* red = gv_smem + (size_t)p.B * p.K;      // [GV_WARPS][B][32*C]
+  for (int idx = threadIdx.x; idx < p.B * p.K; idx += blockDim.x) {
+    const int b = idx / p.K, i = idx % p.K;
+    xin[idx] = p.in[(int64_t)p.in_row[b] * p.in_stride + i];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int col0 = blockIdx.x * 32 * C + lane * C;
+  float acc[MAXB][C];
 #pragma unroll
-      for (int b = 0; b < GV_MAXB; ++b)
-        if (b < p.B) acc[b] = fmaf(p.in[(int64_t)p.in_row[b] * p.in_stride + i], w, acc[b]);
+  for (int b = 0; b < MAXB; ++b)
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[b][c] = 0.f;
+  if (col0 < p.N) {
+#pragma unroll 4
+    for (int i = warp; i < p.K; i += GV_WARPS) {
+      float w[C];
+      GvLoad<TW>::ld(p.W, (int64_t)i * p.N + col0, w);
+#pragma unroll
+      for (int b = 0; b < MAXB; ++b) {
+        if (b < p.B) {
+          const float xv = xin[b * p.K + i];
+#pragma unroll
+          for (int c = 0; c < C; ++c) acc[b][c] = fmaf(xv, w[c], acc[b][c]);
+        }
+      }
     }
   }
 #pragma unroll
-  for (int b = 0; b < GV_MAXB; ++b)
-    if (b < p.B) red[ty][b][tx] = acc[b];
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < p.B * GV_COLS; idx += blockDim.x) {
-    const int b = idx / GV_COLS, c = idx % GV_COLS, oo = blockIdx.x * GV_COLS + c;
-    if (oo >= p.N) continue;
-    float s = red[0][b][c];
+  for (int b = 0; b < MAXB; ++b)
+    if (b < p.B)
 #pragma unroll
-    for (int g = 1; g < GV_KGRP; ++g) s += red[g][b][c];
-    s += p.bias ? p.bias[oo] : 0.f;
-    p.out[(int64_t)b * p.N + oo] = p.act == 1 ? silu_f(s) : s;
+      for (int c = 0; c < C; ++c) red[((size_t)warp * p.B + b) * (32 * C) + lane * C + c] = acc[b][c];
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < p.B * 32 * C; idx += blockDim.x) {
+    const int b = idx / (32 * C), cc = idx % (32 * C);
+    const int o = blockIdx.x * 32 * C + cc;
+    if (o >= p.N) continue;
+    float s = 0.f;
+#pragma unroll
+    for (int g = 0; g < GV_WARPS; ++g) s += red[((size_t)g * p.B + b) * (32 * C) + cc];
+    s += p.bias ? p.bias[o] : 0.f;
+    p.out[(int64_t)b * p.N + o] = p.act == 1 ? silu_f(s) : s;
   }
+}
+
+template <typename TW>
+static size_t gemv_smem(int B, int K) {
+  return ((size_t)B * K + (size_t)GV_WARPS * B * 32 * GvLoad<TW>::C) * sizeof(float);
 }
 
 // ---------------------------------------------------------------- patch embed
@@ -128,30 +177,70 @@ __device__ __forceinline__ void store_act(const LnModArgs& p, int64_t idx, float
   }
 }
 
-static __global__ void ln_mod_kernel(const __grid_constant__ LnModArgs p) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+// one warp per row, the row held in registers (D <= 2048, D % 4 == 0):
+// single read of h, two-pass mean/variance from registers, vector stores.
+constexpr int LN_MAXV = 16;  // float4 per lane
+
+__device__ __forceinline__ void store_act4(const LnModArgs& p, int64_t idx, float4 v) {
+  if (p.out_f32) *reinterpret_cast<float4*>(p.out_f32 + idx) = v;
+  if (p.out_bf16) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&a);
+    u.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(p.out_bf16 + idx) = u;
+  }
+  if (p.out_hi) {
+    float4 hi = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+    *reinterpret_cast<float4*>(p.out_hi + idx) = hi;
+    *reinterpret_cast<float4*>(p.out_lo + idx) =
+        make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);
+  }
+}
+
+static __global__ void __launch_bounds__(256) ln_mod_kernel(const __grid_constant__ LnModArgs p) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (warp >= p.rows) return;
-  const float* hr = p.h + (int64_t)warp * p.D;
+  if (row >= p.rows) return;
+  const int D4 = p.D >> 2;
+  const float4* hr = reinterpret_cast<const float4*>(p.h + (int64_t)row * p.D);
+  float4 v[LN_MAXV];
   float s = 0.f;
-  for (int d = lane; d < p.D; d += 32) s += hr[d];
+#pragma unroll
+  for (int u = 0; u < LN_MAXV; ++u) {
+    const int i = lane + 32 * u;
+    v[u] = i < D4 ? hr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    s += (v[u].x + v[u].y) + (v[u].z + v[u].w);
+  }
 #pragma unroll
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   const float mu = s / p.D;
-  float v = 0.f;
-  for (int d = lane; d < p.D; d += 32) {
-    float t = hr[d] - mu;
-    v = fmaf(t, t, v);
+  float q = 0.f;
+#pragma unroll
+  for (int u = 0; u < LN_MAXV; ++u) {
+    if (lane + 32 * u < D4) {
+      const float a = v[u].x - mu, b = v[u].y - mu, c = v[u].z - mu, d = v[u].w - mu;
+      q = fmaf(a, a, fmaf(b, b, fmaf(c, c, fmaf(d, d, q))));
+    }
   }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  const float rstd = rsqrtf(v / p.D + 1e-6f);
-  const int b = warp / p.L;
-  const float* m = p.mod + (int64_t)b * p.mod_stride;
-  for (int d = lane; d < p.D; d += 32) {
-    float y = (hr[d] - mu) * rstd;
-    y = fmaf(y, 1.f + m[p.scale_off + d], m[p.shift_off + d]);
-    store_act(p, (int64_t)warp * p.D + d, y);
+  for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  const float rstd = rsqrtf(q / p.D + 1e-6f);
+  const int b = row / p.L;
+  const float4* sh = reinterpret_cast<const float4*>(p.mod + (int64_t)b * p.mod_stride + p.shift_off);
+  const float4* sc = reinterpret_cast<const float4*>(p.mod + (int64_t)b * p.mod_stride + p.scale_off);
+#pragma unroll
+  for (int u = 0; u < LN_MAXV; ++u) {
+    const int i = lane + 32 * u;
+    if (i < D4) {
+      const float4 a = sh[i], c = sc[i];
+      float4 y;
+      y.x = fmaf((v[u].x - mu) * rstd, 1.f + c.x, a.x);
+      y.y = fmaf((v[u].y - mu) * rstd, 1.f + c.y, a.y);
+      y.z = fmaf((v[u].z - mu) * rstd, 1.f + c.z, a.z);
+      y.w = fmaf((v[u].w - mu) * rstd, 1.f + c.w, a.w);
+      store_act4(p, (int64_t)row * p.D + 4 * i, y);
+    }
   }
 }
 
@@ -267,6 +356,102 @@ static __global__ void __launch_bounds__(AT_WARPS * 32) attn_kernel(const __grid
       const int d = lane + 32 * u;
       if (u < nU && d < dh) store_act(st, (row0 + q) * p.D + head * dh + d, o_r[r][u] * inv);
     }
+  }
+}
+
+// Whole-sequence attention for short sequences (L <= AS_MAXL): the head's
+// K and V live in smem for the whole CTA, CTA = 16 queries (4 warps x 4), so
+// a (lane, head) pair spreads over L/16 CTAs. Lane j scores keys j + 32m,
+// the probabilities go through a per-warp smem row, lane owns dims lane+32u.
+constexpr int AS_Q = 16, AS_WARPS = 4, AS_MAXL = 512, AS_MAXM = AS_MAXL / 32;
+
+static size_t attn_small_smem(int L, int dh) {
+  return ((size_t)L * (dh + 1) + (size_t)L * dh + AS_Q * dh + AS_WARPS * L) * sizeof(float);
+}
+
+static __global__ void __launch_bounds__(AS_WARPS * 32)
+    attn_small_kernel(const __grid_constant__ AttnArgs p) {
+  extern __shared__ float as_s[];
+  const int dh = p.dh, ldk = dh + 1, L = p.L;
+  float* Ks = as_s;                 // [L][dh+1]
+  float* Vs = Ks + L * ldk;         // [L][dh]
+  float* Qs = Vs + L * dh;          // [AS_Q][dh]
+  float* Ps = Qs + AS_Q * dh;       // [AS_WARPS][L]
+  const int head = blockIdx.y, b = blockIdx.z, q0 = blockIdx.x * AS_Q;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row0 = (int64_t)b * L;
+  const int ld = 3 * p.D;
+  const int dh4 = dh >> 2;  // dh % 4 == 0 (spec heads: 32/64/72/64)
+  for (int idx = threadIdx.x; idx < L * dh4; idx += blockDim.x) {
+    const int j = idx / dh4, d = (idx % dh4) * 4;
+    const float* src = p.qkv + (row0 + j) * ld + head * dh + d;
+    const float4 kv = *reinterpret_cast<const float4*>(src + p.D);
+    const float4 vv = *reinterpret_cast<const float4*>(src + 2 * p.D);
+    float* kd = Ks + j * ldk + d;
+    kd[0] = kv.x; kd[1] = kv.y; kd[2] = kv.z; kd[3] = kv.w;
+    *reinterpret_cast<float4*>(Vs + j * dh + d) = vv;
+  }
+  for (int idx = threadIdx.x; idx < AS_Q * dh; idx += blockDim.x) {
+    const int r = idx / dh, d = idx % dh, q = q0 + r;
+    Qs[idx] = q < L ? p.qkv[(row0 + q) * ld + head * dh + d] * p.scale : 0.f;
+  }
+  __syncthreads();
+  const int nm = (L + 31) / 32;
+  const int nU = (dh + 31) / 32;
+  LnModArgs st{};
+  st.out_f32 = p.out_f32;
+  st.out_bf16 = p.out_bf16;
+  st.out_hi = p.out_hi;
+  st.out_lo = p.out_lo;
+  float* prow = Ps + warp * L;
+  for (int r = 0; r < AS_Q / AS_WARPS; ++r) {
+    const int qr = warp * (AS_Q / AS_WARPS) + r, q = q0 + qr;
+    if (q >= L) break;
+    const float* qv = Qs + qr * dh;
+    float s[AS_MAXM];
+#pragma unroll
+    for (int m = 0; m < AS_MAXM; ++m) s[m] = 0.f;
+    for (int d = 0; d < dh; ++d) {
+      const float x = qv[d];
+#pragma unroll
+      for (int m = 0; m < AS_MAXM; ++m)
+        if (m < nm) s[m] = fmaf(x, Ks[(lane + 32 * m) * ldk + d], s[m]);
+    }
+    float mx = -INFINITY;
+#pragma unroll
+    for (int m = 0; m < AS_MAXM; ++m)
+      if (m < nm && lane + 32 * m < L) mx = fmaxf(mx, s[m]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float sum = 0.f;
+#pragma unroll
+    for (int m = 0; m < AS_MAXM; ++m) {
+      if (m < nm) {
+        const int j = lane + 32 * m;
+        const float e = j < L ? expf(s[m] - mx) : 0.f;
+        if (j < L) prow[j] = e;
+        sum += e;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    __syncwarp();
+    float o_acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int j = 0; j < L; ++j) {
+      const float pj = prow[j];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int d = lane + 32 * u;
+        if (u < nU && d < dh) o_acc[u] = fmaf(pj, Vs[j * dh + d], o_acc[u]);
+      }
+    }
+    const float inv = 1.f / sum;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int d = lane + 32 * u;
+      if (u < nU && d < dh) store_act(st, (row0 + q) * p.D + head * dh + d, o_acc[u] * inv);
+    }
+    __syncwarp();
   }
 }
 

@@ -60,6 +60,76 @@ __device__ __forceinline__ void epi_store(const Epi& e, int m, int n, int N, flo
   }
 }
 
+// 16 consecutive columns n..n+15 of one row (tensor-core epilogue): 16-byte
+// vector loads/stores when the row segment is full and aligned.
+__device__ __forceinline__ void epi_store16(const Epi& e, int m, int n, int N, const float* v) {
+  const bool vec = (n + 16 <= N) && ((N & 3) == 0) && e.mode != EPI_UNPATCH;
+  if (!vec) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (n + j < N) epi_store(e, m, n + j, N, v[j]);
+    return;
+  }
+  const int64_t base = (int64_t)m * N + n;
+  float x[16];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float4 bb = e.bias ? *reinterpret_cast<const float4*>(e.bias + n + 4 * q)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+    x[4 * q] = v[4 * q] + bb.x;
+    x[4 * q + 1] = v[4 * q + 1] + bb.y;
+    x[4 * q + 2] = v[4 * q + 2] + bb.z;
+    x[4 * q + 3] = v[4 * q + 3] + bb.w;
+  }
+  if (e.mode == EPI_STORE) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      *reinterpret_cast<float4*>(e.out + base + 4 * q) =
+          make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+  } else if (e.mode == EPI_GELU) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) x[j] = gelu_tanh_f(x[j]);
+    if (e.out)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<float4*>(e.out + base + 4 * q) =
+            make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+    if (e.out_bf16) {
+      uint32_t u[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(x[2 * q], x[2 * q + 1]);
+        u[q] = *reinterpret_cast<uint32_t*>(&h2);
+      }
+      *reinterpret_cast<uint4*>(e.out_bf16 + base) = make_uint4(u[0], u[1], u[2], u[3]);
+      *reinterpret_cast<uint4*>(e.out_bf16 + base + 8) = make_uint4(u[4], u[5], u[6], u[7]);
+    }
+    if (e.out_hi) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float4 hi = make_float4(tf32_hi(x[4 * q]), tf32_hi(x[4 * q + 1]), tf32_hi(x[4 * q + 2]),
+                                tf32_hi(x[4 * q + 3]));
+        *reinterpret_cast<float4*>(e.out_hi + base + 4 * q) = hi;
+        *reinterpret_cast<float4*>(e.out_lo + base + 4 * q) =
+            make_float4(x[4 * q] - hi.x, x[4 * q + 1] - hi.y, x[4 * q + 2] - hi.z,
+                        x[4 * q + 3] - hi.w);
+      }
+    }
+  } else {  // EPI_RESID
+    const float* g = e.gate + (int64_t)(m / e.L) * e.gate_stride + n;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float4 r = *reinterpret_cast<const float4*>(e.resid + base + 4 * q);
+      const float4 gg = *reinterpret_cast<const float4*>(g + 4 * q);
+      r.x = fmaf(gg.x, x[4 * q], r.x);
+      r.y = fmaf(gg.y, x[4 * q + 1], r.y);
+      r.z = fmaf(gg.z, x[4 * q + 2], r.z);
+      r.w = fmaf(gg.w, x[4 * q + 3], r.w);
+      *reinterpret_cast<float4*>(e.resid + base + 4 * q) = r;
+    }
+  }
+}
+
 constexpr int SG_BM = 64, SG_BN = 64, SG_BK = 16;
 
 static __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict__ A,

@@ -267,13 +267,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   for (int c = 0; c < BN; c += 16) {
     float v[16];
     tmem_ld16(trow + c, v);
-    if (row < M) {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int n = n0 + c + j;
-        if (n < N) epi_store(e, row, n, N, v[j]);
-      }
-    }
+    if (row < M && n0 + c < N) epi_store16(e, row, n0 + c, N, v);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();

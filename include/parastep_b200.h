@@ -158,6 +158,10 @@ int ps_dit_bench_gemm(ps_dit* h, int which, int B, int iters, void* cuda_stream)
 int ps_gemm_test(const float* A, const float* W, const float* bias, float* C, int M, int N, int K,
                  int precision, int impl, void* cuda_stream);
 
+/* Diagnostic: mean device time (us) of `iters` back-to-back tensor-core
+ * GEMM launches on zero operands; dbg bit0 = skip MMA, bit1 = skip TMA. */
+float ps_gemm_probe(int M, int N, int K, int precision, int dbg, int iters);
+
 #ifdef __cplusplus
 }
 #endif

@@ -74,6 +74,7 @@ _SIGS = {
     "ps_dit_flops": (C.c_double, [C.c_void_p]),
     "ps_dit_kernels_per_forward": (C.c_int, [C.c_void_p]),
     "ps_dit_bench_gemm": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]),
+    "ps_gemm_probe": (C.c_float, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
     "ps_gemm_test": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
                                C.c_int, C.c_int, C.c_int, C.c_void_p]),
 }

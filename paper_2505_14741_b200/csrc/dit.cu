@@ -9,6 +9,7 @@
 
 #include "gemm_simt.cuh"
 #include "gemm_tc.cuh"
+#include "attn_mma.cuh"
 
 using namespace ps;
 
@@ -346,7 +347,11 @@ int ps_dit_forward(ps_dit* h, const float* x, const int32_t* host_ts, int B, flo
     e.bias = bw.b_qkv;
     e.out = h->qkv;
     if ((rc = gemm(h, 4 * i + 0, h->a, aop, bw.qkv, M, 3 * D, D, e, st))) return rc;
-    if (small_attn) {
+    if (h->use_tc && h->cfg.precision == 1 && launch_attn_mma(at, B, st)) {
+      // bf16 path: tensor-core flash attention (bf16 MMA)
+    } else if (h->use_tc && h->cfg.precision == 0 && launch_attn_tf32x3(at, B, st)) {
+      // fp32 path: tensor-core flash attention (3xTF32 MMA)
+    } else if (small_attn) {
       dim3 ag((L + AS_Q - 1) / AS_Q, h->H, B);
       attn_small_kernel<<<ag, AS_WARPS * 32, as_smem, st>>>(at);
     } else {

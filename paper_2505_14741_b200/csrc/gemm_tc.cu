@@ -90,6 +90,8 @@ static int alloc_operand(TcActs& acts, TcOperand& op, int rows, int cols, int pr
 
 static int bn_for(int precision, int M) { return (precision == 1 && M > 1024) ? 128 : 64; }
 
+static int g_dbg = 0;  // ps_gemm_probe only
+
 template <int KIND, int BN>
 static int launch(const TcLayer& L, const TcOperand& A, int M, int N, int K, const Epi& e,
                   cudaStream_t st) {
@@ -103,10 +105,10 @@ static int launch(const TcLayer& L, const TcOperand& A, int M, int N, int K, con
   const CUtensorMap& mb = (BN == 128) ? L.map_lo : L.map_main;  // see tc_prepare (bf16 only)
   if (KIND == KIND_BF16)
     gemm_tc_kernel<KIND, BN><<<grid, TC_THREADS, C::SMEM, st>>>(A.map_main, A.map_main, mb, mb, M,
-                                                                 N, K, e);
+                                                                 N, K, e, g_dbg);
   else
     gemm_tc_kernel<KIND, BN><<<grid, TC_THREADS, C::SMEM, st>>>(A.map_main, A.map_lo, L.map_main,
-                                                                 L.map_lo, M, N, K, e);
+                                                                 L.map_lo, M, N, K, e, g_dbg);
   return check_launch("gemm_tc");
 }
 
@@ -224,6 +226,50 @@ int ps_gemm_test(const float* A, const float* W, const float* bias, float* Cout,
   if (!rc && se != cudaSuccess) rc = fail((int)se, std::string("gemm_test: ") + cudaGetErrorString(se));
   tc_release(w, acts);
   return rc;
+}
+
+
+// Diagnostic: average device time (us) of `iters` back-to-back launches of
+// the tensor-core GEMM on zero operands; dbg bit0 skips the MMAs, bit1 the
+// TMA loads (pipeline-isolation experiments). Allocates; not hot path.
+float ps_gemm_probe(int M, int N, int K, int precision, int dbg, int iters) {
+  float *A = nullptr, *W = nullptr, *C = nullptr;
+  if (cudaMalloc(&A, (size_t)M * K * 4) || cudaMalloc(&W, (size_t)K * N * 4) ||
+      cudaMalloc(&C, (size_t)M * N * 4))
+    return -1.f;
+  cudaMemset(A, 0, (size_t)M * K * 4);
+  cudaMemset(W, 0, (size_t)K * N * 4);
+  TcWeights w;
+  TcActs acts;
+  std::vector<const float*> Ws{W};
+  std::vector<int> Ks{K}, Ns{N};
+  float us = -1.f;
+  if (!tc_prepare(w, acts, Ws, Ks, Ns, M, K, K, precision)) {
+    Epi e{};
+    e.mode = EPI_STORE;
+    e.out = C;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    g_dbg = dbg;
+    tc_gemm(w, 0, acts.a, M, N, K, e, precision, 0);
+    cudaEventRecord(a, 0);
+    for (int i = 0; i < iters; ++i) tc_gemm(w, 0, acts.a, M, N, K, e, precision, 0);
+    cudaEventRecord(b, 0);
+    cudaEventSynchronize(b);
+    g_dbg = 0;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    us = ms * 1000.f / iters;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+  cudaDeviceSynchronize();
+  tc_release(w, acts);
+  cudaFree(A);
+  cudaFree(W);
+  cudaFree(C);
+  return us;
 }
 
 }  // extern "C"

@@ -175,7 +175,8 @@ template <int KIND, int BN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapAlo,
                    const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapBlo,
-                   int M, int N, int K, const __grid_constant__ Epi e) {
+                   int M, int N, int K, const __grid_constant__ Epi e, int dbg) {
+  // dbg (diagnostics only, 0 in production): bit0 = no MMA, bit1 = no TMA
   using C = TcCfg<KIND, BN>;
   extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -220,6 +221,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int s = kb % TC_STAGES;
       mbar_wait(&empty[s], ((kb / TC_STAGES) & 1) ^ 1);
       uint8_t* st = smem + s * C::STAGE_BYTES;
+      if (dbg & 2) {
+        mbar_expect_tx(&full[s], 0);
+        continue;
+      }
       mbar_expect_tx(&full[s], C::STAGE_BYTES);
       const int kx = kb * C::BK;
       tma_load_2d(st, &mapA, &full[s], kx, m0);
@@ -239,6 +244,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       uint8_t* st = smem + s * C::STAGE_BYTES;
       const uint64_t a0 = smem_desc_sw128(st);
       const uint64_t b0 = smem_desc_sw128(st + C::A_BYTES);
+      if (dbg & 1) {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+        continue;
+      }
 #pragma unroll
       for (int k = 0; k < C::BK / C::UK; ++k) {
         // advance 32 B along K inside the swizzle atom: +2 in the >>4 address
@@ -254,7 +263,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       umma_commit(&empty[s]);
     }
-    umma_commit(accum);
+    if (dbg & 1)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(accum)) : "memory");
+    else
+      umma_commit(accum);
   }
   __syncwarp();
 

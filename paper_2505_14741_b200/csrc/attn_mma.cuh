@@ -1,23 +1,29 @@
-// Flash attention on tensor cores for the bf16 predictor path.
+// Flash attention on tensor cores (both predictor precisions).
 //
 // softmax(Q K^T / sqrt(dh)) V per (lane b, head), any sequence length L,
-// head_dim dh <= 128 with dh % 8 == 0 (DiT-XL/2: 72, CogVideoX-shaped: 64).
-// CTA = 4 warps x 16 queries; key blocks of 64 staged in smem as bf16
-// (K row-major, V transposed so both MMA B fragments are 32-bit loads);
-// S = Q K^T and O += P V on bf16 MMAs (m16n8k16, fp32 accumulate) with the
-// FA2 register trick (the S accumulator fragment is re-packed in place as
-// the P operand); online softmax in fp32 with exp2. QK^T runs over dh padded
-// to a multiple of 16 with zeros.
-//
+// head_dim dh % 8 == 0 (DiT-S/2 64, DiT-XL/2 72, CogVideoX-shaped 64).
+// CTA = NW warps x 16 queries. Key blocks of 64 rows of K and V are staged
+// fp32 into a 2-stage smem ring with cp.async (16 B, zero-fill past L), so
+// the next block streams in while the current one is on the tensor cores.
+// S = Q K^T and O += P V run on mma.sync with fp32 accumulation; online
+// softmax in fp32; the S accumulator fragment is reused in registers as the
+// P operand (FA2). Two arithmetic modes:
+//   AM_BF16   m16n8k16 bf16 (bf16 path; exp2 with log2e folded into Q)
+//   AM_TF32X3 m16n8k8 tf32 with the 3-pass split x = hi + lo for both MMAs
+//             (fp32 path, error ~1e-6); the S fragment holds columns
+//             {2t, 2t+1} and the tf32 A fragment wants {t, t+4}, so each
+//             8-key group is consumed in the permuted order s(t) = 2t,
+//             s(t+4) = 2t+1 on P and V alike (P.V unchanged, no shuffles).
 // qkv row m = [q(D) | k(D) | v(D)] fp32 from the QKV GEMM; the output row is
-// written in the proj GEMM's operand format (bf16).
+// written in the proj GEMM's operand format.
 #pragma once
 
 #include "dit_kernels.cuh"
 
 namespace ps {
 
-constexpr int FA_WARPS = 4, FA_QW = 16, FA_KB = 64, FA_MAXDH = 128;
+enum { AM_BF16 = 0, AM_TF32X3 = 1 };
+constexpr int FA_QW = 16, FA_KB = 64;
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
@@ -32,200 +38,6 @@ __device__ __forceinline__ void mma_bf16_16816(float* c, const uint32_t* a, cons
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
 }
 
-template <int DHP>  // dh padded to a multiple of 16 (K of QK^T)
-__global__ void __launch_bounds__(FA_WARPS * 32) attn_mma_kernel(const __grid_constant__ AttnArgs p) {
-  constexpr int KST = DHP + 8;        // K smem row stride (bf16), breaks bank conflicts
-  constexpr int VST = FA_KB + 8;      // V^T smem row stride
-  constexpr int NKT = DHP / 16;       // k-steps of QK^T
-  constexpr int NOT = DHP / 8;        // max n-tiles of O (dh/8 used)
-  __shared__ __align__(16) __nv_bfloat16 Ks[FA_KB * KST];
-  __shared__ __align__(16) __nv_bfloat16 Vt[DHP * VST];
-
-  const int dh = p.dh, L = p.L, ld = 3 * p.D;
-  const int head = blockIdx.y, b = blockIdx.z;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gid = lane >> 2, tig = lane & 3;
-  const int64_t row0 = (int64_t)b * L;
-  const int q0 = blockIdx.x * (FA_WARPS * FA_QW) + warp * FA_QW;
-  const float qscale = p.scale * 1.4426950408889634f;  // fold log2(e): softmax via exp2
-
-  // Q fragments (A operand), scaled, zero beyond L / dh
-  uint32_t qa[NKT][4];
-  {
-    const int r0 = q0 + gid, r1 = q0 + gid + 8;
-#pragma unroll
-    for (int ks = 0; ks < NKT; ++ks) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {  // h: column half (k0 or k0+8)
-        const int d = ks * 16 + h * 8 + tig * 2;
-        float a0 = 0.f, a1 = 0.f, c0 = 0.f, c1 = 0.f;
-        if (d < dh) {
-          if (r0 < L) {
-            const float* src = p.qkv + (row0 + r0) * ld + head * dh + d;
-            a0 = src[0] * qscale;
-            a1 = src[1] * qscale;
-          }
-          if (r1 < L) {
-            const float* src = p.qkv + (row0 + r1) * ld + head * dh + d;
-            c0 = src[0] * qscale;
-            c1 = src[1] * qscale;
-          }
-        }
-        qa[ks][2 * h] = pack_bf16(a0, a1);
-        qa[ks][2 * h + 1] = pack_bf16(c0, c1);
-      }
-    }
-  }
-  float o[NOT][4];
-#pragma unroll
-  for (int t = 0; t < NOT; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
-
-  for (int k0 = 0; k0 < L; k0 += FA_KB) {
-    __syncthreads();
-    // stage K (row-major) and V^T for keys k0..k0+63 as bf16, zero padded
-    for (int idx = threadIdx.x; idx < FA_KB * (DHP / 2); idx += blockDim.x) {
-      const int j = idx / (DHP / 2), d = (idx % (DHP / 2)) * 2, kk = k0 + j;
-      float k_a = 0.f, k_b = 0.f, v_a = 0.f, v_b = 0.f;
-      if (kk < L && d < dh) {
-        const float* src = p.qkv + (row0 + kk) * ld + head * dh + d;
-        const float2 kv = *reinterpret_cast<const float2*>(src + p.D);
-        const float2 vv = *reinterpret_cast<const float2*>(src + 2 * p.D);
-        k_a = kv.x; k_b = kv.y; v_a = vv.x; v_b = vv.y;
-      }
-      *reinterpret_cast<uint32_t*>(&Ks[j * KST + d]) = pack_bf16(k_a, k_b);
-      Vt[d * VST + j] = __float2bfloat16_rn(v_a);
-      Vt[(d + 1) * VST + j] = __float2bfloat16_rn(v_b);
-    }
-    __syncthreads();
-    // S = Q K^T : 8 n-tiles of 8 keys
-    float s[FA_KB / 8][4];
-#pragma unroll
-    for (int nt = 0; nt < FA_KB / 8; ++nt) {
-      s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
-#pragma unroll
-      for (int ks = 0; ks < NKT; ++ks) {
-        const __nv_bfloat16* kp = Ks + (nt * 8 + gid) * KST + ks * 16 + tig * 2;
-        uint32_t bfrag[2] = {*reinterpret_cast<const uint32_t*>(kp),
-                             *reinterpret_cast<const uint32_t*>(kp + 8)};
-        mma_bf16_16816(s[nt], qa[ks], bfrag);
-      }
-    }
-    // mask keys beyond L, online softmax (rows gid and gid+8)
-    float mx0 = m0, mx1 = m1;
-#pragma unroll
-    for (int nt = 0; nt < FA_KB / 8; ++nt) {
-      const int kk = k0 + nt * 8 + tig * 2;
-      if (kk >= L) { s[nt][0] = -INFINITY; s[nt][2] = -INFINITY; }
-      if (kk + 1 >= L) { s[nt][1] = -INFINITY; s[nt][3] = -INFINITY; }
-      mx0 = fmaxf(mx0, fmaxf(s[nt][0], s[nt][1]));
-      mx1 = fmaxf(mx1, fmaxf(s[nt][2], s[nt][3]));
-    }
-#pragma unroll
-    for (int o_ = 1; o_ <= 2; o_ <<= 1) {
-      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o_));
-      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o_));
-    }
-    const float c0 = exp2f(m0 - mx0), c1 = exp2f(m1 - mx1);
-    m0 = mx0;
-    m1 = mx1;
-    float rs0 = 0.f, rs1 = 0.f;
-    uint32_t pa[FA_KB / 16][4];
-#pragma unroll
-    for (int nt = 0; nt < FA_KB / 8; ++nt) {
-      const float p0 = exp2f(s[nt][0] - mx0), p1 = exp2f(s[nt][1] - mx0);
-      const float p2 = exp2f(s[nt][2] - mx1), p3 = exp2f(s[nt][3] - mx1);
-      rs0 += p0 + p1;
-      rs1 += p2 + p3;
-      const int kt = nt >> 1, hh = nt & 1;
-      pa[kt][2 * hh] = pack_bf16(p0, p1);
-      pa[kt][2 * hh + 1] = pack_bf16(p2, p3);
-    }
-    l0 = l0 * c0 + rs0;
-    l1 = l1 * c1 + rs1;
-#pragma unroll
-    for (int t = 0; t < NOT; ++t) {
-      o[t][0] *= c0; o[t][1] *= c0;
-      o[t][2] *= c1; o[t][3] *= c1;
-    }
-    // O += P V : k-steps of 16 keys, n-tiles of 8 dims
-#pragma unroll
-    for (int kt = 0; kt < FA_KB / 16; ++kt) {
-#pragma unroll
-      for (int t = 0; t < NOT; ++t) {
-        if (t * 8 < dh) {
-          const __nv_bfloat16* vp = Vt + (t * 8 + gid) * VST + kt * 16 + tig * 2;
-          uint32_t bfrag[2] = {*reinterpret_cast<const uint32_t*>(vp),
-                               *reinterpret_cast<const uint32_t*>(vp + 8)};
-          mma_bf16_16816(o[t], pa[kt], bfrag);
-        }
-      }
-    }
-  }
-  // finalize: row sums across the 4 threads of a row group
-#pragma unroll
-  for (int o_ = 1; o_ <= 2; o_ <<= 1) {
-    l0 += __shfl_xor_sync(0xffffffffu, l0, o_);
-    l1 += __shfl_xor_sync(0xffffffffu, l1, o_);
-  }
-  const float i0 = 1.f / l0, i1 = 1.f / l1;
-  LnModArgs st{};
-  st.out_f32 = p.out_f32;
-  st.out_bf16 = p.out_bf16;
-  st.out_hi = p.out_hi;
-  st.out_lo = p.out_lo;
-  const int r0 = q0 + gid, r1 = q0 + gid + 8;
-#pragma unroll
-  for (int t = 0; t < NOT; ++t) {
-    const int d = t * 8 + tig * 2;
-    if (d < dh) {
-      if (r0 < L) {
-        const int64_t idx = (row0 + r0) * p.D + head * dh + d;
-        store_act(st, idx, o[t][0] * i0);
-        store_act(st, idx + 1, o[t][1] * i0);
-      }
-      if (r1 < L) {
-        const int64_t idx = (row0 + r1) * p.D + head * dh + d;
-        store_act(st, idx, o[t][2] * i1);
-        store_act(st, idx + 1, o[t][3] * i1);
-      }
-    }
-  }
-}
-
-// dispatch on padded head dim; returns false if unsupported
-static inline bool launch_attn_mma(const AttnArgs& a, int B, cudaStream_t st) {
-  const int dhp = (a.dh + 15) / 16 * 16;
-  dim3 grid((a.L + FA_WARPS * FA_QW - 1) / (FA_WARPS * FA_QW), a.H, B);
-  switch (dhp) {
-    case 32: attn_mma_kernel<32><<<grid, FA_WARPS * 32, 0, st>>>(a); return true;
-    case 48: attn_mma_kernel<48><<<grid, FA_WARPS * 32, 0, st>>>(a); return true;
-    case 64: attn_mma_kernel<64><<<grid, FA_WARPS * 32, 0, st>>>(a); return true;
-    case 80: attn_mma_kernel<80><<<grid, FA_WARPS * 32, 0, st>>>(a); return true;
-    case 96: attn_mma_kernel<96><<<grid, FA_WARPS * 32, 0, st>>>(a); return true;
-    case 128: attn_mma_kernel<128><<<grid, FA_WARPS * 32, 0, st>>>(a); return true;
-    default: return false;
-  }
-}
-
-}  // namespace ps
-
-// ---------------------------------------------------------------------------
-// fp32-accurate variant for the fp32 predictor path: the same flash
-// structure on tf32 MMAs (m16n8k8) with the 3-pass split x = hi + lo
-// (hi*hi + hi*lo + lo*hi) for both QK^T and PV. The S accumulator fragment
-// holds columns {2t, 2t+1} while the tf32 A fragment wants {t, t+4}; instead
-// of shuffling, the 8 keys of each group are consumed in the permuted order
-// sigma(t) = 2t, sigma(t+4) = 2t+1 on both P and V, which leaves P.V unchanged.
-namespace ps {
-
-__device__ __forceinline__ uint32_t tf32_bits(float v) { return __float_as_uint(v) & 0xFFFFE000u; }
-
-__device__ __forceinline__ void split_tf32(float v, uint32_t& hi, uint32_t& lo) {
-  hi = tf32_bits(v);
-  lo = __float_as_uint(v - __uint_as_float(hi));
-}
-
 __device__ __forceinline__ void mma_tf32_1688(float* c, const uint32_t* a, const uint32_t* b) {
   asm volatile(
       "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
@@ -234,6 +46,12 @@ __device__ __forceinline__ void mma_tf32_1688(float* c, const uint32_t* a, const
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
 }
 
+__device__ __forceinline__ void split_tf32(float v, uint32_t& hi, uint32_t& lo) {
+  hi = __float_as_uint(v) & 0xFFFFE000u;
+  lo = __float_as_uint(v - __uint_as_float(hi));
+}
+
+// small terms first: lo*hi + hi*lo + hi*hi
 __device__ __forceinline__ void mma3(float* c, const uint32_t* ah, const uint32_t* al,
                                      const uint32_t* bh, const uint32_t* bl) {
   mma_tf32_1688(c, al, bh);
@@ -241,38 +59,83 @@ __device__ __forceinline__ void mma3(float* c, const uint32_t* ah, const uint32_
   mma_tf32_1688(c, ah, bh);
 }
 
-template <int DHP>  // dh padded to a multiple of 8
-__global__ void __launch_bounds__(FA_WARPS * 32) attn_tf32x3_kernel(const __grid_constant__ AttnArgs p) {
-  constexpr int KST = DHP + 4;   // K smem row stride (floats): conflict-free frag loads
-  constexpr int VST = FA_KB + 8; // V^T row stride (floats)
-  constexpr int NKT = DHP / 8;
-  constexpr int NOT = DHP / 8;
-  __shared__ __align__(16) float Ks[FA_KB * KST];
-  __shared__ __align__(16) float Vt[DHP * VST];
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int DHP>
+struct FaCfg {
+  static constexpr int ST = DHP + 4;                 // smem row stride (floats), 16 B multiple
+  static constexpr int STAGE = 2 * FA_KB * ST;       // K block + V block (floats)
+  static constexpr size_t SMEM = 2 * STAGE * sizeof(float);
+};
+
+template <int MODE, int DHP, int NW>
+__global__ void __launch_bounds__(NW * 32) attn_tc_kernel(const __grid_constant__ AttnArgs p) {
+  using C = FaCfg<DHP>;
+  constexpr int ST = C::ST;
+  constexpr int NOT = DHP / 8;  // output n-tiles (only t*8 < dh used)
+  extern __shared__ __align__(16) float fa_smem[];
+  pdl_wait_and_release();
 
   const int dh = p.dh, L = p.L, ld = 3 * p.D;
   const int head = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const int64_t row0 = (int64_t)b * L;
-  const int q0 = blockIdx.x * (FA_WARPS * FA_QW) + warp * FA_QW;
+  const int q0 = blockIdx.x * (NW * FA_QW) + warp * FA_QW;
+  const int nkb = (L + FA_KB - 1) / FA_KB;
+  const int dh4 = dh >> 2;
 
-  uint32_t qh[NKT][4], ql[NKT][4];
-  {
-    const int r0 = q0 + gid, r1 = q0 + gid + 8;
+  // zero the pad columns [dh, DHP) of both stages once (cp.async never writes them)
+  if (DHP > dh) {
+    for (int idx = threadIdx.x; idx < 2 * 2 * FA_KB; idx += NW * 32)
+      for (int d = dh; d < DHP; ++d) fa_smem[idx * ST + d] = 0.f;
+  }
+  auto stage_load = [&](int kb, int stg) {
+    float* Kd = fa_smem + stg * C::STAGE;
+    float* Vd = Kd + FA_KB * ST;
+    for (int idx = threadIdx.x; idx < FA_KB * dh4; idx += NW * 32) {
+      const int j = idx / dh4, c4 = (idx % dh4) * 4, kk = kb * FA_KB + j;
+      const int ok = kk < L ? 16 : 0;
+      const float* src = p.qkv + (row0 + (kk < L ? kk : 0)) * ld + head * dh + c4;
+      cp_async16(Kd + j * ST + c4, src + p.D, ok);
+      cp_async16(Vd + j * ST + c4, src + 2 * p.D, ok);
+    }
+    cp_async_commit();
+  };
+  stage_load(0, 0);
+
+  // Q fragments, pre-scaled (bf16: log2e folded in for exp2 softmax)
+  const float qscale = MODE == AM_BF16 ? p.scale * 1.4426950408889634f : p.scale;
+  const int r0 = q0 + gid, r1 = q0 + gid + 8;
+  auto qval = [&](int r, int d) -> float {
+    return (r < L && d < dh) ? p.qkv[(row0 + r) * ld + head * dh + d] * qscale : 0.f;
+  };
+  constexpr int NKS = MODE == AM_BF16 ? DHP / 16 : DHP / 8;  // k-steps of QK^T
+  uint32_t qh[NKS][4], ql[MODE == AM_BF16 ? 1 : NKS][4];
 #pragma unroll
-    for (int ks = 0; ks < NKT; ++ks) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {  // a0/a1: col tig, a2/a3: col tig+4
-        const int d = ks * 8 + tig + 4 * h;
-        float v0 = 0.f, v1 = 0.f;
-        if (d < dh) {
-          if (r0 < L) v0 = p.qkv[(row0 + r0) * ld + head * dh + d] * p.scale;
-          if (r1 < L) v1 = p.qkv[(row0 + r1) * ld + head * dh + d] * p.scale;
-        }
-        split_tf32(v0, qh[ks][2 * h], ql[ks][2 * h]);
-        split_tf32(v1, qh[ks][2 * h + 1], ql[ks][2 * h + 1]);
-      }
+  for (int ks = 0; ks < NKS; ++ks) {
+    if constexpr (MODE == AM_BF16) {
+      const int d = ks * 16 + tig * 2;
+      qh[ks][0] = pack_bf16(qval(r0, d), qval(r0, d + 1));
+      qh[ks][1] = pack_bf16(qval(r1, d), qval(r1, d + 1));
+      qh[ks][2] = pack_bf16(qval(r0, d + 8), qval(r0, d + 9));
+      qh[ks][3] = pack_bf16(qval(r1, d + 8), qval(r1, d + 9));
+    } else {
+      const int d = ks * 8 + tig;
+      split_tf32(qval(r0, d), qh[ks][0], ql[ks][0]);
+      split_tf32(qval(r1, d), qh[ks][1], ql[ks][1]);
+      split_tf32(qval(r0, d + 4), qh[ks][2], ql[ks][2]);
+      split_tf32(qval(r1, d + 4), qh[ks][3], ql[ks][3]);
     }
   }
   float o[NOT][4];
@@ -280,34 +143,36 @@ __global__ void __launch_bounds__(FA_WARPS * 32) attn_tf32x3_kernel(const __grid
   for (int t = 0; t < NOT; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
 
-  for (int k0 = 0; k0 < L; k0 += FA_KB) {
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < FA_KB * (DHP / 4); idx += blockDim.x) {
-      const int j = idx / (DHP / 4), d = (idx % (DHP / 4)) * 4, kk = k0 + j;
-      float4 kv = make_float4(0.f, 0.f, 0.f, 0.f), vv = kv;
-      if (kk < L && d < dh) {
-        const float* src = p.qkv + (row0 + kk) * ld + head * dh + d;
-        kv = *reinterpret_cast<const float4*>(src + p.D);
-        vv = *reinterpret_cast<const float4*>(src + 2 * p.D);
-      }
-      *reinterpret_cast<float4*>(&Ks[j * KST + d]) = kv;
-      Vt[(d + 0) * VST + j] = vv.x;
-      Vt[(d + 1) * VST + j] = vv.y;
-      Vt[(d + 2) * VST + j] = vv.z;
-      Vt[(d + 3) * VST + j] = vv.w;
+  for (int kb = 0; kb < nkb; ++kb) {
+    if (kb + 1 < nkb) {
+      stage_load(kb + 1, (kb + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
+    const float* Ks = fa_smem + (kb & 1) * C::STAGE;
+    const float* Vs = Ks + FA_KB * ST;
+    const int k0 = kb * FA_KB;
+
     float s[FA_KB / 8][4];
 #pragma unroll
     for (int nt = 0; nt < FA_KB / 8; ++nt) {
       s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+      const float* kr = Ks + (nt * 8 + gid) * ST;
 #pragma unroll
-      for (int ks = 0; ks < NKT; ++ks) {
-        const float* kp = Ks + (nt * 8 + gid) * KST + ks * 8 + tig;
-        uint32_t bh[2], bl[2];
-        split_tf32(kp[0], bh[0], bl[0]);
-        split_tf32(kp[4], bh[1], bl[1]);
-        mma3(s[nt], qh[ks], ql[ks], bh, bl);
+      for (int ks = 0; ks < NKS; ++ks) {
+        if constexpr (MODE == AM_BF16) {
+          const float2 a = *reinterpret_cast<const float2*>(kr + ks * 16 + tig * 2);
+          const float2 c = *reinterpret_cast<const float2*>(kr + ks * 16 + 8 + tig * 2);
+          uint32_t bf[2] = {pack_bf16(a.x, a.y), pack_bf16(c.x, c.y)};
+          mma_bf16_16816(s[nt], qh[ks], bf);
+        } else {
+          uint32_t bh[2], bl[2];
+          split_tf32(kr[ks * 8 + tig], bh[0], bl[0]);
+          split_tf32(kr[ks * 8 + tig + 4], bh[1], bl[1]);
+          mma3(s[nt], qh[ks], ql[ks], bh, bl);
+        }
       }
     }
     float mx0 = m0, mx1 = m1;
@@ -324,41 +189,68 @@ __global__ void __launch_bounds__(FA_WARPS * 32) attn_tf32x3_kernel(const __grid
       mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o_));
       mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o_));
     }
-    const float c0 = expf(m0 - mx0), c1 = expf(m1 - mx1);
+    const float c0 = MODE == AM_BF16 ? exp2f(m0 - mx0) : expf(m0 - mx0);
+    const float c1 = MODE == AM_BF16 ? exp2f(m1 - mx1) : expf(m1 - mx1);
     m0 = mx0;
     m1 = mx1;
-    float rs0 = 0.f, rs1 = 0.f;
 #pragma unroll
     for (int t = 0; t < NOT; ++t) {
       o[t][0] *= c0; o[t][1] *= c0;
       o[t][2] *= c1; o[t][3] *= c1;
     }
+    float rs0 = 0.f, rs1 = 0.f;
+    if constexpr (MODE == AM_BF16) {
+      uint32_t pa[FA_KB / 16][4];
 #pragma unroll
-    for (int nt = 0; nt < FA_KB / 8; ++nt) {
-      const float p0 = expf(s[nt][0] - mx0), p1 = expf(s[nt][1] - mx0);
-      const float p2 = expf(s[nt][2] - mx1), p3 = expf(s[nt][3] - mx1);
-      rs0 += p0 + p1;
-      rs1 += p2 + p3;
-      // A fragment in the permuted key order: a0 = P[g][2t], a1 = P[g+8][2t],
-      // a2 = P[g][2t+1], a3 = P[g+8][2t+1]
-      uint32_t ah[4], al[4];
-      split_tf32(p0, ah[0], al[0]);
-      split_tf32(p2, ah[1], al[1]);
-      split_tf32(p1, ah[2], al[2]);
-      split_tf32(p3, ah[3], al[3]);
+      for (int nt = 0; nt < FA_KB / 8; ++nt) {
+        const float p0 = exp2f(s[nt][0] - mx0), p1 = exp2f(s[nt][1] - mx0);
+        const float p2 = exp2f(s[nt][2] - mx1), p3 = exp2f(s[nt][3] - mx1);
+        rs0 += p0 + p1;
+        rs1 += p2 + p3;
+        pa[nt >> 1][2 * (nt & 1)] = pack_bf16(p0, p1);
+        pa[nt >> 1][2 * (nt & 1) + 1] = pack_bf16(p2, p3);
+      }
 #pragma unroll
-      for (int t = 0; t < NOT; ++t) {
-        if (t * 8 < dh) {
-          const float2 v2 = *reinterpret_cast<const float2*>(Vt + (t * 8 + gid) * VST + nt * 8 + tig * 2);
-          uint32_t bh[2], bl[2];
-          split_tf32(v2.x, bh[0], bl[0]);  // key 2t   (A column t)
-          split_tf32(v2.y, bh[1], bl[1]);  // key 2t+1 (A column t+4)
-          mma3(o[t], ah, al, bh, bl);
+      for (int kt = 0; kt < FA_KB / 16; ++kt) {
+        const float* v0 = Vs + (kt * 16 + tig * 2) * ST;
+#pragma unroll
+        for (int t = 0; t < NOT; ++t) {
+          if (t * 8 < dh) {
+            const int d = t * 8 + gid;
+            uint32_t bf[2] = {pack_bf16(v0[d], v0[ST + d]),
+                              pack_bf16(v0[8 * ST + d], v0[9 * ST + d])};
+            mma_bf16_16816(o[t], pa[kt], bf);
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int nt = 0; nt < FA_KB / 8; ++nt) {
+        const float p0 = expf(s[nt][0] - mx0), p1 = expf(s[nt][1] - mx0);
+        const float p2 = expf(s[nt][2] - mx1), p3 = expf(s[nt][3] - mx1);
+        rs0 += p0 + p1;
+        rs1 += p2 + p3;
+        uint32_t ah[4], al[4];  // permuted order: a0 = P[g][2t], a2 = P[g][2t+1]
+        split_tf32(p0, ah[0], al[0]);
+        split_tf32(p2, ah[1], al[1]);
+        split_tf32(p1, ah[2], al[2]);
+        split_tf32(p3, ah[3], al[3]);
+        const float* v0 = Vs + (nt * 8 + tig * 2) * ST;
+#pragma unroll
+        for (int t = 0; t < NOT; ++t) {
+          if (t * 8 < dh) {
+            const int d = t * 8 + gid;
+            uint32_t bh[2], bl[2];
+            split_tf32(v0[d], bh[0], bl[0]);       // key 2t   (A column t)
+            split_tf32(v0[ST + d], bh[1], bl[1]);  // key 2t+1 (A column t+4)
+            mma3(o[t], ah, al, bh, bl);
+          }
         }
       }
     }
     l0 = l0 * c0 + rs0;
     l1 = l1 * c1 + rs1;
+    __syncthreads();  // the stage is overwritten by the next prefetch
   }
 #pragma unroll
   for (int o_ = 1; o_ <= 2; o_ <<= 1) {
@@ -371,7 +263,6 @@ __global__ void __launch_bounds__(FA_WARPS * 32) attn_tf32x3_kernel(const __grid
   st.out_bf16 = p.out_bf16;
   st.out_hi = p.out_hi;
   st.out_lo = p.out_lo;
-  const int r0 = q0 + gid, r1 = q0 + gid + 8;
 #pragma unroll
   for (int t = 0; t < NOT; ++t) {
     const int d = t * 8 + tig * 2;
@@ -390,13 +281,36 @@ __global__ void __launch_bounds__(FA_WARPS * 32) attn_tf32x3_kernel(const __grid
   }
 }
 
-static inline bool launch_attn_tf32x3(const AttnArgs& a, int B, cudaStream_t st) {
-  const int dhp = (a.dh + 7) / 8 * 8;
-  dim3 grid((a.L + FA_WARPS * FA_QW - 1) / (FA_WARPS * FA_QW), a.H, B);
-  switch (dhp) {
-    case 32: attn_tf32x3_kernel<32><<<grid, FA_WARPS * 32, 0, st>>>(a); return true;
-    case 64: attn_tf32x3_kernel<64><<<grid, FA_WARPS * 32, 0, st>>>(a); return true;
-    case 72: attn_tf32x3_kernel<72><<<grid, FA_WARPS * 32, 0, st>>>(a); return true;
+constexpr int FA_NW = 2;  // 32 queries per CTA: more CTAs for short sequences
+
+template <int MODE, int DHP>
+static inline void launch_fa(const AttnArgs& a, int B, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_tc_kernel<MODE, DHP, FA_NW>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FaCfg<DHP>::SMEM);
+    attr = true;
+  }
+  dim3 grid((a.L + FA_NW * FA_QW - 1) / (FA_NW * FA_QW), a.H, B);
+  launch_pdl(attn_tc_kernel<MODE, DHP, FA_NW>, grid, dim3(FA_NW * 32), FaCfg<DHP>::SMEM, st, a);
+}
+
+// mode AM_BF16 / AM_TF32X3; returns false for unsupported head dims
+static inline bool launch_attn_tc(int mode, const AttnArgs& a, int B, cudaStream_t st) {
+  if (a.dh % 8) return false;
+  if (mode == AM_BF16) {
+    switch ((a.dh + 15) / 16 * 16) {
+      case 32: launch_fa<AM_BF16, 32>(a, B, st); return true;
+      case 64: launch_fa<AM_BF16, 64>(a, B, st); return true;
+      case 80: launch_fa<AM_BF16, 80>(a, B, st); return true;
+      case 128: launch_fa<AM_BF16, 128>(a, B, st); return true;
+      default: return false;
+    }
+  }
+  switch (a.dh) {
+    case 32: launch_fa<AM_TF32X3, 32>(a, B, st); return true;
+    case 64: launch_fa<AM_TF32X3, 64>(a, B, st); return true;
+    case 72: launch_fa<AM_TF32X3, 72>(a, B, st); return true;
     default: return false;
   }
 }

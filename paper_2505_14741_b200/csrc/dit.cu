@@ -60,7 +60,8 @@ template <typename TW, int MAXB>
 static void gemv_launch(const GemvArgs& p, cudaStream_t st) {
   constexpr int C = GvLoad<TW>::C;
   const size_t smem = gemv_smem<TW>(p.B, p.K);
-  gemv_kernel<TW, MAXB><<<(p.N + 32 * C - 1) / (32 * C), GV_WARPS * 32, smem, st>>>(p);
+  launch_pdl(gemv_kernel<TW, MAXB>, dim3((p.N + 32 * C - 1) / (32 * C)), dim3(GV_WARPS * 32), smem,
+             st, p);
 }
 
 template <typename TW>
@@ -119,7 +120,7 @@ static int ln_mod(ps_dit* h, int rows, int shift_off, int scale_off, const TcOpe
     p.out_f32 = h->a;
   }
   const int threads = 256;  // 8 rows per block
-  ln_mod_kernel<<<(rows * 32 + threads - 1) / threads, threads, 0, st>>>(p);
+  launch_pdl(ln_mod_kernel, dim3((rows * 32 + threads - 1) / threads), dim3(threads), 0, st, p);
   return check_launch("ln_mod");
 }
 
@@ -130,7 +131,7 @@ static int gemm(ps_dit* h, int tc_layer, const float* A_f32, const TcOperand* A_
                 int M, int N, int K, const Epi& e, cudaStream_t st) {
   if (h->use_tc) return tc_gemm(h->tcw, tc_layer, *A_tc, M, N, K, e, h->cfg.precision, st);
   dim3 grid((N + SG_BN - 1) / SG_BN, (M + SG_BM - 1) / SG_BM);
-  gemm_simt_kernel<<<grid, 256, 0, st>>>(A_f32, W, M, N, K, e);
+  launch_pdl(gemm_simt_kernel, grid, dim3(256), 0, st, A_f32, W, M, N, K, e);
   return check_launch("gemm_simt");
 }
 
@@ -313,8 +314,8 @@ int ps_dit_forward(ps_dit* h, const float* x, const int32_t* host_ts, int B, flo
   if ((rc = gemv(h->silu_c, D, nullptr, abf ? (const void*)h->Wada_bf16 : (const void*)h->Wada_all,
                  abf, h->bada_all, h->mod, D, h->n_ada, B, 0, st)))
     return rc;
-  patch_embed_kernel<<<M, 128, h->P * sizeof(float), st>>>(x, h->n_latent, h->g, h->P, h->Wpe,
-                                                           h->bpe, h->pos, h->h, B);
+  launch_pdl(patch_embed_kernel, dim3(M), dim3(128), h->P * sizeof(float), st, x, h->n_latent,
+             h->g, h->P, h->Wpe, h->bpe, h->pos, h->h, B);
   if ((rc = check_launch("patch_embed"))) return rc;
 
   const TcOperand* aop = h->use_tc ? &h->tca.a : nullptr;
@@ -347,16 +348,16 @@ int ps_dit_forward(ps_dit* h, const float* x, const int32_t* host_ts, int B, flo
     e.bias = bw.b_qkv;
     e.out = h->qkv;
     if ((rc = gemm(h, 4 * i + 0, h->a, aop, bw.qkv, M, 3 * D, D, e, st))) return rc;
-    if (h->use_tc && h->cfg.precision == 1 && launch_attn_mma(at, B, st)) {
+    if (h->use_tc && h->cfg.precision == 1 && launch_attn_tc(AM_BF16, at, B, st)) {
       // bf16 path: tensor-core flash attention (bf16 MMA)
-    } else if (h->use_tc && h->cfg.precision == 0 && launch_attn_tf32x3(at, B, st)) {
+    } else if (h->use_tc && h->cfg.precision == 0 && launch_attn_tc(AM_TF32X3, at, B, st)) {
       // fp32 path: tensor-core flash attention (3xTF32 MMA)
     } else if (small_attn) {
       dim3 ag((L + AS_Q - 1) / AS_Q, h->H, B);
-      attn_small_kernel<<<ag, AS_WARPS * 32, as_smem, st>>>(at);
+      launch_pdl(attn_small_kernel, ag, dim3(AS_WARPS * 32), as_smem, st, at);
     } else {
       dim3 ag((L + AT_Q - 1) / AT_Q, h->H, B);
-      attn_kernel<<<ag, AT_WARPS * 32, at_smem, st>>>(at);
+      launch_pdl(attn_kernel, ag, dim3(AT_WARPS * 32), at_smem, st, at);
     }
     if ((rc = check_launch("attn"))) return rc;
     e = Epi{};

@@ -75,6 +75,7 @@ template <> struct GvLoad<__nv_bfloat16> {
 template <typename TW, int MAXB>
 __global__ void __launch_bounds__(GV_WARPS * 32) gemv_kernel(const __grid_constant__ GemvArgs p) {
   constexpr int C = GvLoad<TW>::C;
+  pdl_wait_and_release();
   extern __shared__ float gv_smem[];
   float* xin = gv_smem;                          // [B][K]
   float* red = gv_smem + (size_t)p.B * p.K;      // [GV_WARPS][B][32*C]
@@ -135,6 +136,7 @@ static __global__ void patch_embed_kernel(const float* __restrict__ x, int64_t n
                                    const float* __restrict__ bpe, const float* __restrict__ pos,
                                    float* __restrict__ h, int B) {
   extern __shared__ float patch_s[];  // patch_dim values of this token
+  pdl_wait_and_release();
   const int row = blockIdx.x;  // b*L + l
   const int b = row / g.L, l = row % g.L;
   for (int k = threadIdx.x; k < patch_dim; k += blockDim.x)
@@ -199,6 +201,7 @@ __device__ __forceinline__ void store_act4(const LnModArgs& p, int64_t idx, floa
 }
 
 static __global__ void __launch_bounds__(256) ln_mod_kernel(const __grid_constant__ LnModArgs p) {
+  pdl_wait_and_release();
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= p.rows) return;
@@ -263,6 +266,7 @@ struct AttnArgs {
 
 static __global__ void __launch_bounds__(AT_WARPS * 32) attn_kernel(const __grid_constant__ AttnArgs p) {
   extern __shared__ float at_s[];
+  pdl_wait_and_release();
   const int dh = p.dh, ldk = dh + 1;
   float* Ks = at_s;                // [AT_K][ldk]
   float* Vs = Ks + AT_K * ldk;     // [AT_K][dh]
@@ -372,6 +376,7 @@ static size_t attn_small_smem(int L, int dh) {
 static __global__ void __launch_bounds__(AS_WARPS * 32)
     attn_small_kernel(const __grid_constant__ AttnArgs p) {
   extern __shared__ float as_s[];
+  pdl_wait_and_release();
   const int dh = p.dh, ldk = dh + 1, L = p.L;
   float* Ks = as_s;                 // [L][dh+1]
   float* Vs = Ks + L * ldk;         // [L][dh]

@@ -137,6 +137,7 @@ static __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __re
                                                        int K, const __grid_constant__ Epi e) {
   __shared__ float As[SG_BK][SG_BM + 4];
   __shared__ float Bs[SG_BK][SG_BN + 4];
+  pdl_wait_and_release();
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   const int m0 = blockIdx.y * SG_BM, n0 = blockIdx.x * SG_BN;
   float acc[4][4] = {};

@@ -103,12 +103,14 @@ static int launch(const TcLayer& L, const TcOperand& A, int M, int N, int K, con
   });
   dim3 grid((N + BN - 1) / BN, (M + TC_BM - 1) / TC_BM);
   const CUtensorMap& mb = (BN == 128) ? L.map_lo : L.map_main;  // see tc_prepare (bf16 only)
+  cudaError_t err;
   if (KIND == KIND_BF16)
-    gemm_tc_kernel<KIND, BN><<<grid, TC_THREADS, C::SMEM, st>>>(A.map_main, A.map_main, mb, mb, M,
-                                                                 N, K, e, g_dbg);
+    err = launch_pdl(gemm_tc_kernel<KIND, BN>, grid, dim3(TC_THREADS), (size_t)C::SMEM, st,
+                     A.map_main, A.map_main, mb, mb, M, N, K, e, g_dbg);
   else
-    gemm_tc_kernel<KIND, BN><<<grid, TC_THREADS, C::SMEM, st>>>(A.map_main, A.map_lo, L.map_main,
-                                                                 L.map_lo, M, N, K, e, g_dbg);
+    err = launch_pdl(gemm_tc_kernel<KIND, BN>, grid, dim3(TC_THREADS), (size_t)C::SMEM, st,
+                     A.map_main, A.map_lo, L.map_main, L.map_lo, M, N, K, e, g_dbg);
+  if (err != cudaSuccess) return fail((int)err, std::string("gemm_tc: ") + cudaGetErrorString(err));
   return check_launch("gemm_tc");
 }
 

@@ -189,6 +189,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * BN;
   const int nk = (K + C::BK - 1) / C::BK;
+  if (dbg & 8) return;  // probe: launch floor only
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&mapA);
@@ -214,6 +215,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  // the prologue above overlaps the predecessor's tail (PDL); operands and
+  // epilogue inputs are only touched after it completes
+  pdl_wait_and_release();
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer
@@ -279,7 +283,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   for (int c = 0; c < BN; c += 16) {
     float v[16];
     tmem_ld16(trow + c, v);
-    if (row < M && n0 + c < N) epi_store16(e, row, n0 + c, N, v);
+    if ((dbg & 4) == 0 && row < M && n0 + c < N) epi_store16(e, row, n0 + c, N, v);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();

@@ -106,6 +106,7 @@ constexpr int ZCACHE = 7;  // roll steps whose z stays in registers (degree <= 8
 
 template <typename T, int VEC, bool SCALAR>
 __global__ void __launch_bounds__(256) cycle_kernel(const __grid_constant__ CycleParams p) {
+  pdl_wait_and_release();
   const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * VEC;
   if (i0 >= p.n) return;
   const int cnt = (p.n - i0) < VEC ? (int)(p.n - i0) : VEC;
@@ -114,11 +115,21 @@ __global__ void __launch_bounds__(256) cycle_kernel(const __grid_constant__ Cycl
   Vec<T, VEC, SCALAR> x;
   x.load(p.x_in, i0, cnt);
   double z[VEC];
-  for (int k = 0; k < p.n_apply; ++k) {
+  // issue the first PF eps loads up front (independent 16 B loads in flight:
+  // the kernel is HBM-bound at large n and latency-bound otherwise)
+  constexpr int PF = 8;
+  Vec<T, VEC, SCALAR> ev[PF];
+#pragma unroll
+  for (int k = 0; k < PF; ++k)
+    if (k < p.n_apply) ev[k].load(p.eps[k], i0, cnt);
+#pragma unroll
+  for (int k = 0; k < PS_MAX_CYCLE; ++k) {
+    if (k >= p.n_apply) break;
     const ps_step s = p.apply[k];
     if (p.rec[k]) x.store(p.rec[k], i0, cnt);
     Vec<T, VEC, SCALAR> e;
-    e.load(p.eps[k], i0, cnt);
+    if (k < PF) e = ev[k];
+    else e.load(p.eps[k], i0, cnt);
     if (s.noisy) gen_z<VEC>(seed, s.t, i0, z);
     step_vec(x, e, s, z);
   }
@@ -185,16 +196,21 @@ __global__ void rng_uniform_kernel(T* out, int64_t n, uint64_t key, uint64_t c0,
 template <typename T>
 static int launch_cycle(const CycleParams& p, cudaStream_t st, bool vec_ok) {
   constexpr int VEC = 16 / sizeof(T);
+  cudaError_t e;
+  // small latents (e.g. 4096 elements): 64-thread blocks spread over more SMs
   if (vec_ok) {
     int64_t threads = (p.n + VEC - 1) / VEC;
-    unsigned blocks = (unsigned)((threads + 255) / 256);
-    cycle_kernel<T, VEC, false><<<blocks, 256, 0, st>>>(p);
+    const int bs = threads >= 148 * 512 ? 256 : 64;
+    unsigned blocks = (unsigned)((threads + bs - 1) / bs);
+    e = launch_pdl(cycle_kernel<T, VEC, false>, dim3(blocks), dim3(bs), 0, st, p);
   } else {
     // unaligned buffers: 2 elements per thread, scalar loads
     int64_t threads = (p.n + 1) / 2;
-    unsigned blocks = (unsigned)((threads + 255) / 256);
-    cycle_kernel<T, 2, true><<<blocks, 256, 0, st>>>(p);
+    const int bs = threads >= 148 * 512 ? 256 : 64;
+    unsigned blocks = (unsigned)((threads + bs - 1) / bs);
+    e = launch_pdl(cycle_kernel<T, 2, true>, dim3(blocks), dim3(bs), 0, st, p);
   }
+  if (e != cudaSuccess) return fail((int)e, std::string("cycle_kernel: ") + cudaGetErrorString(e));
   return check_launch("cycle_kernel");
 }
 

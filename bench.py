@@ -136,7 +136,7 @@ def run_cfg(cfg, n, degree, strategy=None):
     from paper_2505_14741_b200.engines import RunConfig
 
     if strategy is None:
-        strategy = "sequential" if degree == 1 else "parastep"
+        strategy = "sequential" if (degree == 1 and not USE_NCCL) else "parastep"
     return RunConfig(steps=cfg["T"], warmup=cfg["warmup"] if degree > 1 else 0,
                      strategy=strategy, degree=degree, seed=0, data_dim=n)
 
@@ -274,8 +274,11 @@ def config_block(args, cfg, world):
 
 
 # ------------------------------------------------------------------ GPU arm
+USE_NCCL = False  # set in main(): world > 1, or --force-nccl (1-rank NCCL path check)
+
+
 def make_sampler(w, sched, rcfg, world, record=False, external_init=False):
-    if world == 1:
+    if world == 1 and not (USE_NCCL and rcfg.strategy == "parastep"):
         from paper_2505_14741_b200.engines import DeviceSampler
 
         return DeviceSampler(w, sched, rcfg, record=record, external_init=external_init)
@@ -423,11 +426,11 @@ def our_arm(args, cfg, world, rank, local):
             dist.barrier()
         t0 = time.perf_counter()
         e2s.run(i, graph=True, x_init=x_host)
-        if world == 1:
+        if hasattr(e2s, "trajectory"):
             tr = e2s.trajectory()
             assert tr.steps == cfg["T"]
         else:
-            res = e2s.result()
+            res = e2s.result()  # rank 0: full Trajectory; others: x0
             assert res.x0.shape[0] == n
         dt = (time.perf_counter() - t0) * 1e3
         if i >= args.warmup:
@@ -509,6 +512,8 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=3,
                     help="reference arm: sampler steps timed per bench step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-nccl", action="store_true",
+                    help="run the NCCL rank loop even at one rank (path check under torchrun)")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if world != args.gpus:
@@ -517,7 +522,9 @@ def main():
     if args.impl == "reference":
         reference_arm(args, cfg, world, rank)
         return
-    if world > 1:
+    global USE_NCCL
+    USE_NCCL = world > 1 or args.force_nccl
+    if USE_NCCL:
         import torch
         import torch.distributed as dist
 
@@ -526,7 +533,7 @@ def main():
     try:
         our_arm(args, cfg, world, rank, local)
     finally:
-        if world > 1:
+        if USE_NCCL:
             import torch.distributed as dist
 
             dist.destroy_process_group()

@@ -241,7 +241,7 @@ int ps_dit_create(const ps_dit_config* cfg, const ps_dit_weights* w, ps_dit** ou
       Ws.push_back(bw.fc2); Ks.push_back(h->Dm); Ns.push_back(D);
     }
     Ws.push_back(h->Wfo); Ks.push_back(D); Ns.push_back(h->P);
-    rc = tc_prepare(h->tcw, h->tca, Ws, Ks, Ns, (int)BL, D, h->Dm, cfg->precision);
+    rc = tc_prepare(h->tcw, h->tca, Ws, Ks, Ns, (int)BL, h->L, D, h->Dm, cfg->precision);
     if (rc) {
       ps_dit_destroy(h);
       return rc;

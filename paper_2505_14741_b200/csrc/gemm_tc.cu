@@ -88,41 +88,65 @@ static int alloc_operand(TcActs& acts, TcOperand& op, int rows, int cols, int pr
   return make_map(&op.map_lo, op.lo, 4, cols, rows, TC_BM);
 }
 
-static int bn_for(int precision, int M) { return (precision == 1 && M > 1024) ? 128 : 64; }
-
 static int g_dbg = 0;  // ps_gemm_probe only
 
 template <int KIND, int BN>
-static int launch(const TcLayer& L, const TcOperand& A, int M, int N, int K, const Epi& e,
-                  cudaStream_t st) {
+static int launch(const TcWeights& w, const TcLayer& L, const TcOperand& A, int M, int N, int K,
+                  const Epi& e, cudaStream_t st) {
   using C = TcCfg<KIND, BN>;
   static std::once_flag once;
   std::call_once(once, [] {
     cudaFuncSetAttribute(gemm_tc_kernel<KIND, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          C::SMEM);
   });
-  dim3 grid((N + BN - 1) / BN, (M + TC_BM - 1) / TC_BM);
+  const int tiles_n = (N + BN - 1) / BN, tiles_m = (M + TC_BM - 1) / TC_BM;
+  TcSplit sk{1, nullptr, nullptr};
+  if (L.splits > 1 && w.ws && (size_t)L.splits * tiles_n * tiles_m * TC_BM * BN <= w.ws_floats &&
+      tiles_n * tiles_m <= w.max_tiles)
+    sk = TcSplit{L.splits, w.ws, w.counter};
+  dim3 grid(tiles_n, tiles_m, sk.splits);
   const CUtensorMap& mb = (BN == 128) ? L.map_lo : L.map_main;  // see tc_prepare (bf16 only)
   cudaError_t err;
   if (KIND == KIND_BF16)
     err = launch_pdl(gemm_tc_kernel<KIND, BN>, grid, dim3(TC_THREADS), (size_t)C::SMEM, st,
-                     A.map_main, A.map_main, mb, mb, M, N, K, e, g_dbg);
+                     A.map_main, A.map_main, mb, mb, M, N, K, e, g_dbg, sk);
   else
     err = launch_pdl(gemm_tc_kernel<KIND, BN>, grid, dim3(TC_THREADS), (size_t)C::SMEM, st,
-                     A.map_main, A.map_lo, L.map_main, L.map_lo, M, N, K, e, g_dbg);
+                     A.map_main, A.map_lo, L.map_main, L.map_lo, M, N, K, e, g_dbg, sk);
   if (err != cudaSuccess) return fail((int)err, std::string("gemm_tc: ") + cudaGetErrorString(err));
   return check_launch("gemm_tc");
 }
 
+// split-K factor from the one-lane shape (ref_rows): enough CTAs to cover
+// the 148 SMs while every split keeps >= 4 K-blocks. Fixed per layer so a
+// row's accumulation order never depends on the batch.
+static int choose_splits(int ref_rows, int N, int K, int bk) {
+  const int tiles = ((ref_rows + TC_BM - 1) / TC_BM) * ((N + 63) / 64);
+  const int nk = (K + bk - 1) / bk;
+  int s = 1;
+  while (s < 8 && tiles * s * 2 <= 148 && nk / (s * 2) >= 4) s *= 2;
+  return s;
+}
+
 int tc_prepare(TcWeights& w, TcActs& acts, const std::vector<const float*>& Ws,
-               const std::vector<int>& Ks, const std::vector<int>& Ns, int max_rows, int D, int Dm,
-               int precision) {
+               const std::vector<int>& Ks, const std::vector<int>& Ns, int max_rows, int ref_rows,
+               int D, int Dm, int precision) {
   w.precision = precision;
   w.layers.resize(Ws.size());
+  const int bk = precision == 1 ? TcCfg<KIND_BF16, 64>::BK : TcCfg<KIND_TF32X3, 64>::BK;
+  size_t ws_floats = 0;
+  int max_tiles = 0;
   for (size_t i = 0; i < Ws.size(); ++i) {
     TcLayer& L = w.layers[i];
     L.K = Ks[i];
     L.N = Ns[i];
+    L.splits = choose_splits(ref_rows, L.N, L.K, bk);
+    const int tiles = ((max_rows + TC_BM - 1) / TC_BM) * ((L.N + 63) / 64);
+    max_tiles = tiles > max_tiles ? tiles : max_tiles;
+    if (L.splits > 1) {
+      const size_t need = (size_t)L.splits * tiles * TC_BM * 64;
+      ws_floats = need > ws_floats ? need : ws_floats;
+    }
     const size_t n = (size_t)L.K * L.N;
     PS_CHECK_ARG(L.K % 8 == 0, "tensor-core GEMM needs K % 8 == 0");
     cudaError_t e;
@@ -148,6 +172,14 @@ int tc_prepare(TcWeights& w, TcActs& acts, const std::vector<const float*>& Ws,
       if (int rc = make_map(&L.map_lo, L.w_lo, 4, L.K, L.N, 64)) return rc;
     }
   }
+  if (ws_floats) {
+    if (cudaMalloc(&w.ws, ws_floats * 4) != cudaSuccess ||
+        cudaMalloc(&w.counter, (size_t)max_tiles * sizeof(int)) != cudaSuccess)
+      return fail(PS_ECUDA, "cudaMalloc split-K workspace");
+    cudaMemset(w.counter, 0, (size_t)max_tiles * sizeof(int));
+    w.ws_floats = ws_floats;
+    w.max_tiles = max_tiles;
+  }
   if (int rc = alloc_operand(acts, acts.a, max_rows, D, precision)) return rc;
   if (int rc = alloc_operand(acts, acts.o, max_rows, D, precision)) return rc;
   if (int rc = alloc_operand(acts, acts.hid, max_rows, Dm, precision)) return rc;
@@ -157,11 +189,8 @@ int tc_prepare(TcWeights& w, TcActs& acts, const std::vector<const float*>& Ws,
 int tc_gemm(const TcWeights& w, int layer, const TcOperand& A, int M, int N, int K, const Epi& e,
             int precision, cudaStream_t st) {
   const TcLayer& L = w.layers[layer];
-  if (precision == 1) {
-    if (bn_for(precision, M) == 128) return launch<KIND_BF16, 128>(L, A, M, N, K, e, st);
-    return launch<KIND_BF16, 64>(L, A, M, N, K, e, st);
-  }
-  return launch<KIND_TF32X3, 64>(L, A, M, N, K, e, st);
+  if (precision == 1) return launch<KIND_BF16, 64>(w, L, A, M, N, K, e, st);
+  return launch<KIND_TF32X3, 64>(w, L, A, M, N, K, e, st);
 }
 
 void tc_release(TcWeights& w, TcActs& acts) {
@@ -170,6 +199,10 @@ void tc_release(TcWeights& w, TcActs& acts) {
     if (L.w_lo) cudaFree(L.w_lo);
   }
   w.layers.clear();
+  if (w.ws) cudaFree(w.ws);
+  if (w.counter) cudaFree(w.counter);
+  w.ws = nullptr;
+  w.counter = nullptr;
   for (void* p : acts.owned) cudaFree(p);
   acts.owned.clear();
 }
@@ -216,7 +249,7 @@ int ps_gemm_test(const float* A, const float* W, const float* bias, float* Cout,
   TcActs acts;
   std::vector<const float*> Ws{W};
   std::vector<int> Ks{K}, Ns{N};
-  int rc = tc_prepare(w, acts, Ws, Ks, Ns, M, K, K, precision);
+  int rc = tc_prepare(w, acts, Ws, Ks, Ns, M, M, K, K, precision);
   if (!rc) {
     const int64_t n = (int64_t)M * K;
     convert_act_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(A, acts.a.bf16, acts.a.hi,
@@ -246,7 +279,7 @@ float ps_gemm_probe(int M, int N, int K, int precision, int dbg, int iters) {
   std::vector<const float*> Ws{W};
   std::vector<int> Ks{K}, Ns{N};
   float us = -1.f;
-  if (!tc_prepare(w, acts, Ws, Ks, Ns, M, K, K, precision)) {
+  if (!tc_prepare(w, acts, Ws, Ks, Ns, M, M, K, K, precision)) {
     Epi e{};
     e.mode = EPI_STORE;
     e.out = C;

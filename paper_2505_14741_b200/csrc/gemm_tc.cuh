@@ -48,11 +48,16 @@ struct TcLayer {
   void* w_lo = nullptr;    // tf32-lo fp32 [N][K]
   CUtensorMap map_main, map_lo;
   int bn;
+  int splits = 1;  // split-K factor, fixed per layer (independent of M: batch == single bitwise)
 };
 
 struct TcWeights {
   std::vector<TcLayer> layers;
   int precision = 0;
+  float* ws = nullptr;       // split-K partial tiles
+  int* counter = nullptr;    // split-K arrival counters (zero between launches)
+  size_t ws_floats = 0;
+  int max_tiles = 0;
 };
 
 constexpr int TC_BM = 128;
@@ -171,11 +176,22 @@ struct TcCfg {
   static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
 };
 
+// Deterministic split-K (small-M GEMMs have few output tiles): blockIdx.z
+// takes K-blocks [z*nk/S, (z+1)*nk/S); every split stores its fp32 partial
+// tile to `ws`, the last split to arrive at the tile's counter sums the S
+// partials in split order 0..S-1 (order fixed, arrival order irrelevant) and
+// runs the fused epilogue, then re-arms the counter for the next launch.
+struct TcSplit {
+  int splits;
+  float* ws;     // [splits][tiles][TC_BM * BN]
+  int* counter;  // [tiles], zero between launches
+};
+
 template <int KIND, int BN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapAlo,
                    const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapBlo,
-                   int M, int N, int K, const __grid_constant__ Epi e, int dbg) {
+                   int M, int N, int K, const __grid_constant__ Epi e, int dbg, TcSplit sk) {
   // dbg (diagnostics only, 0 in production): bit0 = no MMA, bit1 = no TMA
   using C = TcCfg<KIND, BN>;
   extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
@@ -185,10 +201,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* empty = full + TC_STAGES;
   uint64_t* accum = empty + TC_STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * BN;
-  const int nk = (K + C::BK - 1) / C::BK;
+  const int nk_all = (K + C::BK - 1) / C::BK;
+  const int kb0 = (int)((int64_t)blockIdx.z * nk_all / sk.splits);
+  const int kb1 = (int)((int64_t)(blockIdx.z + 1) * nk_all / sk.splits);
+  const int nk = kb1 - kb0;
   if (dbg & 8) return;  // probe: launch floor only
 
   if (threadIdx.x == 0) {
@@ -230,7 +250,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         continue;
       }
       mbar_expect_tx(&full[s], C::STAGE_BYTES);
-      const int kx = kb * C::BK;
+      const int kx = (kb0 + kb) * C::BK;
       tma_load_2d(st, &mapA, &full[s], kx, m0);
       tma_load_2d(st + C::A_BYTES, &mapB, &full[s], kx, n0);
       if (KIND == KIND_TF32X3) {
@@ -279,11 +299,54 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const int row = m0 + warp * 32 + lane;
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  if (sk.splits == 1) {
 #pragma unroll 1
-  for (int c = 0; c < BN; c += 16) {
-    float v[16];
-    tmem_ld16(trow + c, v);
-    if ((dbg & 4) == 0 && row < M && n0 + c < N) epi_store16(e, row, n0 + c, N, v);
+    for (int c = 0; c < BN; c += 16) {
+      float v[16];
+      tmem_ld16(trow + c, v);
+      if ((dbg & 4) == 0 && row < M && n0 + c < N) epi_store16(e, row, n0 + c, N, v);
+    }
+  } else {
+    const int tiles = gridDim.x * gridDim.y;
+    const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+    const int rloc = warp * 32 + lane;
+    float* mine = sk.ws + ((size_t)blockIdx.z * tiles + tile) * (TC_BM * BN) + (size_t)rloc * BN;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 16) {
+      float v[16];
+      tmem_ld16(trow + c, v);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<float4*>(mine + c + 4 * q) =
+            make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) *last_flag = (atomicAdd(sk.counter + tile, 1) == sk.splits - 1);
+    __syncthreads();
+    if (*last_flag) {
+      __threadfence();
+      const float* part = sk.ws + (size_t)tile * (TC_BM * BN) + (size_t)rloc * BN;
+      const size_t sstride = (size_t)tiles * (TC_BM * BN);
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        float v[16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 a = __ldcg(reinterpret_cast<const float4*>(part + c + 4 * q));
+          v[4 * q] = a.x; v[4 * q + 1] = a.y; v[4 * q + 2] = a.z; v[4 * q + 3] = a.w;
+        }
+        for (int s = 1; s < sk.splits; ++s) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float4 a = __ldcg(reinterpret_cast<const float4*>(part + s * sstride + c + 4 * q));
+            v[4 * q] += a.x; v[4 * q + 1] += a.y; v[4 * q + 2] += a.z; v[4 * q + 3] += a.w;
+          }
+        }
+        if (row < M && n0 + c < N) epi_store16(e, row, n0 + c, N, v);
+      }
+      if (threadIdx.x == 0) sk.counter[tile] = 0;  // re-arm for the next launch / replay
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -295,8 +358,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
 // ------------------------------------------------------------------ host side
 int tc_prepare(TcWeights& w, TcActs& acts, const std::vector<const float*>& Ws,
-               const std::vector<int>& Ks, const std::vector<int>& Ns, int max_rows, int D, int Dm,
-               int precision);
+               const std::vector<int>& Ks, const std::vector<int>& Ns, int max_rows, int ref_rows,
+               int D, int Dm, int precision);
 int tc_gemm(const TcWeights& w, int layer, const TcOperand& A, int M, int N, int K, const Epi& e,
             int precision, cudaStream_t st);
 void tc_release(TcWeights& w, TcActs& acts);

@@ -1,0 +1,8 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout -s KILL 600 python -m pytest tests/test_gpu_dit.py tests/test_gpu_sampler.py tests/test_gpu_nccl.py -q -x 2>&1 | tail -15 > gpurun_out/r6_tests.log
+timeout -s KILL 300 python tools/gemm_probe.py > gpurun_out/r6_probe.txt 2>&1
+timeout -s KILL 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/r6_bench.json 2> gpurun_out/r6_bench.err
+timeout -s KILL 600 python bench.py --config dit_xl2_bf16 --steps 3 --warmup 2 --batchstep 4 --no-cpu-baseline > gpurun_out/r6_bench_xl.json 2> gpurun_out/r6_bench_xl.err
+timeout -s KILL 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29611 bench.py --gpus 1 --steps 3 --warmup 2 --force-nccl --no-cpu-baseline --batchstep > gpurun_out/r6_bench_nccl.json 2> gpurun_out/r6_bench_nccl.err
+timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r6_launches_dits2.csv python tools/profile_denoise.py --config small_dit_fp32 > gpurun_out/r6_ncu1.log 2>&1

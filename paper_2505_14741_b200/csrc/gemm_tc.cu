@@ -89,10 +89,13 @@ static int alloc_operand(TcActs& acts, TcOperand& op, int rows, int cols, int pr
 }
 
 static int g_dbg = 0;  // ps_gemm_probe only
+static int g_split_enable = 1;  // probe bit 5 disables cluster split-K
+
+static int bn_index(int bn) { return bn == 32 ? 0 : (bn == 64 ? 1 : 2); }
 
 template <int KIND, int BN>
-static int launch(const TcWeights& w, const TcLayer& L, const TcOperand& A, int M, int N, int K,
-                  const Epi& e, cudaStream_t st) {
+static int launch(const TcLayer& L, const TcOperand& A, int M, int N, int K, const Epi& e,
+                  cudaStream_t st) {
   using C = TcCfg<KIND, BN>;
   static std::once_flag once;
   std::call_once(once, [] {
@@ -100,32 +103,53 @@ static int launch(const TcWeights& w, const TcLayer& L, const TcOperand& A, int 
                          C::SMEM);
   });
   const int tiles_n = (N + BN - 1) / BN, tiles_m = (M + TC_BM - 1) / TC_BM;
-  TcSplit sk{1, nullptr, nullptr};
-  if (L.splits > 1 && w.ws && (size_t)L.splits * tiles_n * tiles_m * TC_BM * BN <= w.ws_floats &&
-      tiles_n * tiles_m <= w.max_tiles)
-    sk = TcSplit{L.splits, w.ws, w.counter};
-  dim3 grid(tiles_n, tiles_m, sk.splits);
-  const CUtensorMap& mb = (BN == 128) ? L.map_lo : L.map_main;  // see tc_prepare (bf16 only)
+  const TcSplit sk{L.splits};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(tiles_n, tiles_m, sk.splits);
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = 1;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = sk.splits;
+  cfg.attrs = at;
+  cfg.numAttrs = sk.splits > 1 ? 2 : 1;
+  const int bi = bn_index(BN);
   cudaError_t err;
   if (KIND == KIND_BF16)
-    err = launch_pdl(gemm_tc_kernel<KIND, BN>, grid, dim3(TC_THREADS), (size_t)C::SMEM, st,
-                     A.map_main, A.map_main, mb, mb, M, N, K, e, g_dbg, sk);
+    err = cudaLaunchKernelEx(&cfg, gemm_tc_kernel<KIND, BN>, A.map_main, A.map_main, L.map_b[bi],
+                             L.map_b[bi], M, N, K, e, g_dbg, sk);
   else
-    err = launch_pdl(gemm_tc_kernel<KIND, BN>, grid, dim3(TC_THREADS), (size_t)C::SMEM, st,
-                     A.map_main, A.map_lo, L.map_main, L.map_lo, M, N, K, e, g_dbg, sk);
+    err = cudaLaunchKernelEx(&cfg, gemm_tc_kernel<KIND, BN>, A.map_main, A.map_lo, L.map_b[bi],
+                             L.map_blo[bi], M, N, K, e, g_dbg, sk);
   if (err != cudaSuccess) return fail((int)err, std::string("gemm_tc: ") + cudaGetErrorString(err));
   return check_launch("gemm_tc");
 }
 
-// split-K factor from the one-lane shape (ref_rows): enough CTAs to cover
-// the 148 SMs while every split keeps >= 4 K-blocks. Fixed per layer so a
-// row's accumulation order never depends on the batch.
+// Split-K factor from the one-lane shape (ref_rows) with 64-wide tiles: grow
+// the cluster while it still fits the 148 SMs and every split keeps >= 4
+// K-blocks. Fixed per layer, so a row's accumulation order never depends on
+// the batch (forward_batch == mapped forward, bitwise).
 static int choose_splits(int ref_rows, int N, int K, int bk) {
   const int tiles = ((ref_rows + TC_BM - 1) / TC_BM) * ((N + 63) / 64);
   const int nk = (K + bk - 1) / bk;
   int s = 1;
   while (s < 8 && tiles * s * 2 <= 148 && nk / (s * 2) >= 4) s *= 2;
-  return s;
+  return g_split_enable ? s : 1;
+}
+
+// N-tile width per call: narrow 32-wide tiles when the grid would cover at
+// most half the SMs, 128-wide (bf16) for large grids. Any width gives the
+// same per-element accumulation order.
+static int choose_bn(int precision, int M, int N, int splits) {
+  const int t64 = ((M + TC_BM - 1) / TC_BM) * ((N + 63) / 64);
+  if (t64 * splits <= 74) return 32;
+  if (precision == 1 && t64 > 600) return 128;
+  return 64;
 }
 
 int tc_prepare(TcWeights& w, TcActs& acts, const std::vector<const float*>& Ws,
@@ -134,19 +158,11 @@ int tc_prepare(TcWeights& w, TcActs& acts, const std::vector<const float*>& Ws,
   w.precision = precision;
   w.layers.resize(Ws.size());
   const int bk = precision == 1 ? TcCfg<KIND_BF16, 64>::BK : TcCfg<KIND_TF32X3, 64>::BK;
-  size_t ws_floats = 0;
-  int max_tiles = 0;
   for (size_t i = 0; i < Ws.size(); ++i) {
     TcLayer& L = w.layers[i];
     L.K = Ks[i];
     L.N = Ns[i];
     L.splits = choose_splits(ref_rows, L.N, L.K, bk);
-    const int tiles = ((max_rows + TC_BM - 1) / TC_BM) * ((L.N + 63) / 64);
-    max_tiles = tiles > max_tiles ? tiles : max_tiles;
-    if (L.splits > 1) {
-      const size_t need = (size_t)L.splits * tiles * TC_BM * 64;
-      ws_floats = need > ws_floats ? need : ws_floats;
-    }
     const size_t n = (size_t)L.K * L.N;
     PS_CHECK_ARG(L.K % 8 == 0, "tensor-core GEMM needs K % 8 == 0");
     cudaError_t e;
@@ -163,22 +179,15 @@ int tc_prepare(TcWeights& w, TcActs& acts, const std::vector<const float*>& Ws,
         Ws[i], L.K, L.N, precision == 1 ? (__nv_bfloat16*)L.w_main : nullptr,
         precision == 1 ? nullptr : (float*)L.w_main, precision == 1 ? nullptr : (float*)L.w_lo);
     if (int rc = check_launch("transpose_convert")) return rc;
-    if (precision == 1) {
-      // bf16: map_main boxes 64 rows of N, map_lo (reused slot) boxes 128
-      if (int rc = make_map(&L.map_main, L.w_main, 2, L.K, L.N, 64)) return rc;
-      if (int rc = make_map(&L.map_lo, L.w_main, 2, L.K, L.N, 128)) return rc;
-    } else {
-      if (int rc = make_map(&L.map_main, L.w_main, 4, L.K, L.N, 64)) return rc;
-      if (int rc = make_map(&L.map_lo, L.w_lo, 4, L.K, L.N, 64)) return rc;
+    const int boxes[3] = {32, 64, 128};
+    for (int bi = 0; bi < 3; ++bi) {
+      if (precision == 1) {
+        if (int rc = make_map(&L.map_b[bi], L.w_main, 2, L.K, L.N, boxes[bi])) return rc;
+      } else if (bi < 2) {
+        if (int rc = make_map(&L.map_b[bi], L.w_main, 4, L.K, L.N, boxes[bi])) return rc;
+        if (int rc = make_map(&L.map_blo[bi], L.w_lo, 4, L.K, L.N, boxes[bi])) return rc;
+      }
     }
-  }
-  if (ws_floats) {
-    if (cudaMalloc(&w.ws, ws_floats * 4) != cudaSuccess ||
-        cudaMalloc(&w.counter, (size_t)max_tiles * sizeof(int)) != cudaSuccess)
-      return fail(PS_ECUDA, "cudaMalloc split-K workspace");
-    cudaMemset(w.counter, 0, (size_t)max_tiles * sizeof(int));
-    w.ws_floats = ws_floats;
-    w.max_tiles = max_tiles;
   }
   if (int rc = alloc_operand(acts, acts.a, max_rows, D, precision)) return rc;
   if (int rc = alloc_operand(acts, acts.o, max_rows, D, precision)) return rc;
@@ -189,8 +198,14 @@ int tc_prepare(TcWeights& w, TcActs& acts, const std::vector<const float*>& Ws,
 int tc_gemm(const TcWeights& w, int layer, const TcOperand& A, int M, int N, int K, const Epi& e,
             int precision, cudaStream_t st) {
   const TcLayer& L = w.layers[layer];
-  if (precision == 1) return launch<KIND_BF16, 64>(w, L, A, M, N, K, e, st);
-  return launch<KIND_TF32X3, 64>(w, L, A, M, N, K, e, st);
+  const int bn = choose_bn(precision, M, N, L.splits);
+  if (precision == 1) {
+    if (bn == 32) return launch<KIND_BF16, 32>(L, A, M, N, K, e, st);
+    if (bn == 128) return launch<KIND_BF16, 128>(L, A, M, N, K, e, st);
+    return launch<KIND_BF16, 64>(L, A, M, N, K, e, st);
+  }
+  if (bn == 32) return launch<KIND_TF32X3, 32>(L, A, M, N, K, e, st);
+  return launch<KIND_TF32X3, 64>(L, A, M, N, K, e, st);
 }
 
 void tc_release(TcWeights& w, TcActs& acts) {
@@ -199,10 +214,6 @@ void tc_release(TcWeights& w, TcActs& acts) {
     if (L.w_lo) cudaFree(L.w_lo);
   }
   w.layers.clear();
-  if (w.ws) cudaFree(w.ws);
-  if (w.counter) cudaFree(w.counter);
-  w.ws = nullptr;
-  w.counter = nullptr;
   for (void* p : acts.owned) cudaFree(p);
   acts.owned.clear();
 }
@@ -268,6 +279,8 @@ int ps_gemm_test(const float* A, const float* W, const float* bias, float* Cout,
 // the tensor-core GEMM on zero operands; dbg bit0 skips the MMAs, bit1 the
 // TMA loads (pipeline-isolation experiments). Allocates; not hot path.
 float ps_gemm_probe(int M, int N, int K, int precision, int dbg, int iters) {
+  g_split_enable = (dbg & 32) ? 0 : 1;  // bit 5: disable cluster split-K
+  dbg &= 15;
   float *A = nullptr, *W = nullptr, *C = nullptr;
   if (cudaMalloc(&A, (size_t)M * K * 4) || cudaMalloc(&W, (size_t)K * N * 4) ||
       cudaMalloc(&C, (size_t)M * N * 4))
@@ -304,6 +317,7 @@ float ps_gemm_probe(int M, int N, int K, int precision, int dbg, int iters) {
   cudaFree(A);
   cudaFree(W);
   cudaFree(C);
+  g_split_enable = 1;
   return us;
 }
 

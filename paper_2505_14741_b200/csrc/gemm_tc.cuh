@@ -46,18 +46,15 @@ struct TcLayer {
   int K, N;
   void* w_main = nullptr;  // bf16 [N][K] or tf32-hi fp32 [N][K]
   void* w_lo = nullptr;    // tf32-lo fp32 [N][K]
-  CUtensorMap map_main, map_lo;
-  int bn;
+  // B operand maps per N-tile width (index 0: 32 rows, 1: 64, 2: 128); *_lo
+  // are the tf32-lo copies of the 3xTF32 path
+  CUtensorMap map_b[3], map_blo[3];
   int splits = 1;  // split-K factor, fixed per layer (independent of M: batch == single bitwise)
 };
 
 struct TcWeights {
   std::vector<TcLayer> layers;
   int precision = 0;
-  float* ws = nullptr;       // split-K partial tiles
-  int* counter = nullptr;    // split-K arrival counters (zero between launches)
-  size_t ws_floats = 0;
-  int max_tiles = 0;
 };
 
 constexpr int TC_BM = 128;
@@ -176,16 +173,33 @@ struct TcCfg {
   static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
 };
 
-// Deterministic split-K (small-M GEMMs have few output tiles): blockIdx.z
-// takes K-blocks [z*nk/S, (z+1)*nk/S); every split stores its fp32 partial
-// tile to `ws`, the last split to arrive at the tile's counter sums the S
-// partials in split order 0..S-1 (order fixed, arrival order irrelevant) and
-// runs the fused epilogue, then re-arms the counter for the next launch.
+// Deterministic split-K for small-M GEMMs (few output tiles): the S splits
+// of a tile form one thread-block cluster (1, 1, S). Split z takes K-blocks
+// [z*nk/S, (z+1)*nk/S), parks its fp32 partial tile in its own smem (the
+// drained stage ring), and after a cluster barrier CTA z reduces rows
+// [z*128/S, (z+1)*128/S) by reading all S partials over DSMEM in split order
+// 0..S-1 (fixed order: bit-reproducible) and runs the fused epilogue.
 struct TcSplit {
   int splits;
-  float* ws;     // [splits][tiles][TC_BM * BN]
-  int* counter;  // [tiles], zero between launches
 };
+
+__device__ __forceinline__ float4 ld_dsmem_f4(const float* local, uint32_t cta) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+               : "=r"(remote)
+               : "r"(smem_u32(local)), "r"(cta));
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(remote)
+               : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
 
 template <int KIND, int BN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -201,7 +215,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* empty = full + TC_STAGES;
   uint64_t* accum = empty + TC_STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
-  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * BN;
@@ -307,46 +320,40 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       if ((dbg & 4) == 0 && row < M && n0 + c < N) epi_store16(e, row, n0 + c, N, v);
     }
   } else {
-    const int tiles = gridDim.x * gridDim.y;
-    const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+    // partial tile -> own smem (stage ring is drained: all MMAs completed)
+    constexpr int PST = BN + 4;  // row stride (floats), keeps 16-B alignment
+    float* part = reinterpret_cast<float*>(smem);
     const int rloc = warp * 32 + lane;
-    float* mine = sk.ws + ((size_t)blockIdx.z * tiles + tile) * (TC_BM * BN) + (size_t)rloc * BN;
 #pragma unroll 1
     for (int c = 0; c < BN; c += 16) {
       float v[16];
       tmem_ld16(trow + c, v);
 #pragma unroll
       for (int q = 0; q < 4; ++q)
-        *reinterpret_cast<float4*>(mine + c + 4 * q) =
+        *reinterpret_cast<float4*>(part + rloc * PST + c + 4 * q) =
             make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     }
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) *last_flag = (atomicAdd(sk.counter + tile, 1) == sk.splits - 1);
-    __syncthreads();
-    if (*last_flag) {
-      __threadfence();
-      const float* part = sk.ws + (size_t)tile * (TC_BM * BN) + (size_t)rloc * BN;
-      const size_t sstride = (size_t)tiles * (TC_BM * BN);
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
-        float v[16];
+    cluster_sync_all();
+    const int S = sk.splits, rows = TC_BM / S, r0 = blockIdx.z * rows;
+    const int chunks = rows * (BN / 16);
+    for (int idx = threadIdx.x; idx < chunks; idx += TC_THREADS) {
+      const int r = r0 + idx / (BN / 16), c = (idx % (BN / 16)) * 16;
+      float v[16];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 a = ld_dsmem_f4(part + r * PST + c + 4 * q, 0);
+        v[4 * q] = a.x; v[4 * q + 1] = a.y; v[4 * q + 2] = a.z; v[4 * q + 3] = a.w;
+      }
+      for (int s = 1; s < S; ++s) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const float4 a = __ldcg(reinterpret_cast<const float4*>(part + c + 4 * q));
-          v[4 * q] = a.x; v[4 * q + 1] = a.y; v[4 * q + 2] = a.z; v[4 * q + 3] = a.w;
+          const float4 a = ld_dsmem_f4(part + r * PST + c + 4 * q, (uint32_t)s);
+          v[4 * q] += a.x; v[4 * q + 1] += a.y; v[4 * q + 2] += a.z; v[4 * q + 3] += a.w;
         }
-        for (int s = 1; s < sk.splits; ++s) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float4 a = __ldcg(reinterpret_cast<const float4*>(part + s * sstride + c + 4 * q));
-            v[4 * q] += a.x; v[4 * q + 1] += a.y; v[4 * q + 2] += a.z; v[4 * q + 3] += a.w;
-          }
-        }
-        if (row < M && n0 + c < N) epi_store16(e, row, n0 + c, N, v);
       }
-      if (threadIdx.x == 0) sk.counter[tile] = 0;  // re-arm for the next launch / replay
+      if (m0 + r < M && n0 + c < N) epi_store16(e, m0 + r, n0 + c, N, v);
     }
+    cluster_sync_all();  // peers' smem stays live until every CTA has read it
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();

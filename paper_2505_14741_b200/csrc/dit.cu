@@ -119,7 +119,8 @@ static int ln_mod(ps_dit* h, int rows, int shift_off, int scale_off, const TcOpe
   } else {
     p.out_f32 = h->a;
   }
-  const int threads = 256;  // 8 rows per block
+  // 2 rows (warps) per block: a 256-token lane spreads over 128 SMs
+  const int threads = rows >= 148 * 16 ? 256 : 64;
   launch_pdl(ln_mod_kernel, dim3((rows * 32 + threads - 1) / threads), dim3(threads), 0, st, p);
   return check_launch("ln_mod");
 }

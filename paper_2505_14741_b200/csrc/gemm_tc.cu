@@ -89,7 +89,8 @@ static int alloc_operand(TcActs& acts, TcOperand& op, int rows, int cols, int pr
 }
 
 static int g_dbg = 0;  // ps_gemm_probe only
-static int g_split_enable = 1;  // probe bit 5 disables cluster split-K
+static int g_split_enable = 1;  // probe bit 5 disables split-K
+static int g_force_in_cta = 0;  // probe bit 6 runs the segments in-CTA (no cluster)
 
 static int bn_index(int bn) { return bn == 32 ? 0 : (bn == 64 ? 1 : 2); }
 
@@ -103,9 +104,14 @@ static int launch(const TcLayer& L, const TcOperand& A, int M, int N, int K, con
                          C::SMEM);
   });
   const int tiles_n = (N + BN - 1) / BN, tiles_m = (M + TC_BM - 1) / TC_BM;
-  const TcSplit sk{L.splits};
+  // segments as a cluster only while the whole grid is co-resident (clusters
+  // of 4/8 leave some SMs unusable, hence the lower cap); else in-CTA
+  const int tiles = tiles_n * tiles_m;
+  const bool as_cluster =
+      L.splits > 1 && tiles * L.splits <= (L.splits == 2 ? 148 : 128) && !g_force_in_cta;
+  const TcSplit sk{L.splits, as_cluster ? L.splits : 1};
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(tiles_n, tiles_m, sk.splits);
+  cfg.gridDim = dim3(tiles_n, tiles_m, sk.cluster);
   cfg.blockDim = dim3(TC_THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
@@ -115,9 +121,9 @@ static int launch(const TcLayer& L, const TcOperand& A, int M, int N, int K, con
   at[1].id = cudaLaunchAttributeClusterDimension;
   at[1].val.clusterDim.x = 1;
   at[1].val.clusterDim.y = 1;
-  at[1].val.clusterDim.z = sk.splits;
+  at[1].val.clusterDim.z = sk.cluster;
   cfg.attrs = at;
-  cfg.numAttrs = sk.splits > 1 ? 2 : 1;
+  cfg.numAttrs = sk.cluster > 1 ? 2 : 1;
   const int bi = bn_index(BN);
   cudaError_t err;
   if (KIND == KIND_BF16)
@@ -138,7 +144,7 @@ static int choose_splits(int ref_rows, int N, int K, int bk) {
   const int tiles = ((ref_rows + TC_BM - 1) / TC_BM) * ((N + 63) / 64);
   const int nk = (K + bk - 1) / bk;
   int s = 1;
-  while (s < 8 && tiles * s * 2 <= 148 && nk / (s * 2) >= 4) s *= 2;
+  while (s < 8 && tiles * s * 2 <= (s == 1 ? 148 : 128) && nk / (s * 2) >= 4) s *= 2;
   return g_split_enable ? s : 1;
 }
 
@@ -147,8 +153,9 @@ static int choose_splits(int ref_rows, int N, int K, int bk) {
 // same per-element accumulation order.
 static int choose_bn(int precision, int M, int N, int splits) {
   const int t64 = ((M + TC_BM - 1) / TC_BM) * ((N + 63) / 64);
-  if (t64 * splits <= 74) return 32;
-  if (precision == 1 && t64 > 600) return 128;
+  const int cap = splits <= 2 ? 148 : 128;  // co-resident CTAs for this cluster size
+  if (2 * t64 * splits <= cap) return 32;
+  if (precision == 1 && t64 > 600 && splits <= 4) return 128;  // TMEM: S x 128 <= 512
   return 64;
 }
 
@@ -247,6 +254,10 @@ int ps_gemm_test(const float* A, const float* W, const float* bias, float* Cout,
                  int K, int precision, int impl, void* cs) {
   PS_CHECK_ARG(M > 0 && N > 0 && K > 0, "bad GEMM shape");
   cudaStream_t st = as_stream(cs);
+  // impl 3: tensor cores with the K segments forced in-CTA (cluster-free);
+  // must equal impl 2 bit-for-bit (test_gemm_split_paths_bitwise)
+  g_force_in_cta = impl == 3 ? 1 : 0;
+  if (impl == 3) impl = 2;
   Epi e{};
   e.mode = EPI_STORE;
   e.bias = bias;
@@ -271,6 +282,7 @@ int ps_gemm_test(const float* A, const float* W, const float* bias, float* Cout,
   cudaError_t se = cudaStreamSynchronize(st);
   if (!rc && se != cudaSuccess) rc = fail((int)se, std::string("gemm_test: ") + cudaGetErrorString(se));
   tc_release(w, acts);
+  g_force_in_cta = 0;
   return rc;
 }
 
@@ -279,7 +291,8 @@ int ps_gemm_test(const float* A, const float* W, const float* bias, float* Cout,
 // the tensor-core GEMM on zero operands; dbg bit0 skips the MMAs, bit1 the
 // TMA loads (pipeline-isolation experiments). Allocates; not hot path.
 float ps_gemm_probe(int M, int N, int K, int precision, int dbg, int iters) {
-  g_split_enable = (dbg & 32) ? 0 : 1;  // bit 5: disable cluster split-K
+  g_split_enable = (dbg & 32) ? 0 : 1;  // bit 5: disable split-K
+  g_force_in_cta = (dbg & 64) ? 1 : 0;  // bit 6: segments in-CTA
   dbg &= 15;
   float *A = nullptr, *W = nullptr, *C = nullptr;
   if (cudaMalloc(&A, (size_t)M * K * 4) || cudaMalloc(&W, (size_t)K * N * 4) ||
@@ -318,6 +331,7 @@ float ps_gemm_probe(int M, int N, int K, int precision, int dbg, int iters) {
   cudaFree(W);
   cudaFree(C);
   g_split_enable = 1;
+  g_force_in_cta = 0;
   return us;
 }
 

@@ -173,14 +173,21 @@ struct TcCfg {
   static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
 };
 
-// Deterministic split-K for small-M GEMMs (few output tiles): the S splits
-// of a tile form one thread-block cluster (1, 1, S). Split z takes K-blocks
-// [z*nk/S, (z+1)*nk/S), parks its fp32 partial tile in its own smem (the
-// drained stage ring), and after a cluster barrier CTA z reduces rows
-// [z*128/S, (z+1)*128/S) by reading all S partials over DSMEM in split order
-// 0..S-1 (fixed order: bit-reproducible) and runs the fused epilogue.
+// Deterministic split-K. A layer's K range is cut into S segments (S fixed
+// per layer, see tc_prepare) and the result is always
+//     acc = ((seg_0 + seg_1) + seg_2) + ...      (each seg_s accumulated in TMEM)
+// whichever way the segments are executed, so a row's bits never depend on
+// the batch:
+//   cluster == S  small M (few tiles): the S segment-CTAs of a tile form a
+//                 thread-block cluster (1, 1, S); each parks its fp32 partial
+//                 tile in its own drained smem ring, and after a cluster
+//                 barrier CTA z reduces rows [z*128/S, (z+1)*128/S) over DSMEM
+//                 in segment order and runs the fused epilogue;
+//   cluster == 1  large M: one CTA runs all S segments into S TMEM
+//                 accumulators and adds them in the same order.
 struct TcSplit {
-  int splits;
+  int splits;   // S: K segments (fixed per layer)
+  int cluster;  // 1 (segments in-CTA) or S (one CTA per segment)
 };
 
 __device__ __forceinline__ float4 ld_dsmem_f4(const float* local, uint32_t cta) {
@@ -219,9 +226,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * BN;
   const int nk_all = (K + C::BK - 1) / C::BK;
-  const int kb0 = (int)((int64_t)blockIdx.z * nk_all / sk.splits);
-  const int kb1 = (int)((int64_t)(blockIdx.z + 1) * nk_all / sk.splits);
+  const int S = sk.splits;
+  const bool in_cta = sk.cluster == 1;  // all segments in this CTA
+  const int kb0 = in_cta ? 0 : (int)((int64_t)blockIdx.z * nk_all / S);
+  const int kb1 = in_cta ? nk_all : (int)((int64_t)(blockIdx.z + 1) * nk_all / S);
   const int nk = kb1 - kb0;
+  // TMEM columns: one BN-wide accumulator per in-CTA segment (power of 2 >= 32)
+  uint32_t tcols = 32;
+  while (tcols < (uint32_t)((in_cta ? S : 1) * BN)) tcols <<= 1;
   if (dbg & 8) return;  // probe: launch floor only
 
   if (threadIdx.x == 0) {
@@ -241,7 +253,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "n"(C::TMEM_COLS));
+                 "r"(tcols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -274,7 +286,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer
     constexpr uint32_t idesc = make_idesc(KIND, TC_BM, BN);
+    int seg = 0, seg_end = in_cta ? (int)((int64_t)nk_all / S) : nk, seg_start = 0;
     for (int kb = 0; kb < nk; ++kb) {
+      if (kb == seg_end) {  // next in-CTA segment: fresh accumulator columns
+        ++seg;
+        seg_start = kb;
+        seg_end = (int)((int64_t)(seg + 1) * nk_all / S);
+      }
+      const uint32_t dacc = tmem + (uint32_t)(seg * BN);
       const int s = kb % TC_STAGES;
       mbar_wait(&full[s], (kb / TC_STAGES) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -289,13 +308,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int k = 0; k < C::BK / C::UK; ++k) {
         // advance 32 B along K inside the swizzle atom: +2 in the >>4 address
         const uint64_t koff = (uint64_t)(k * C::UK * C::ESZ) >> 4;
-        const uint32_t acc = (kb | k) ? 1u : 0u;
-        umma<KIND>(tmem, a0 + koff, b0 + koff, idesc, acc);
+        const uint32_t acc = ((kb - seg_start) | k) ? 1u : 0u;
+        umma<KIND>(dacc, a0 + koff, b0 + koff, idesc, acc);
         if constexpr (KIND == KIND_TF32X3) {
           const uint64_t alo = smem_desc_sw128(st + C::A_BYTES + C::B_BYTES);
           const uint64_t blo = smem_desc_sw128(st + 2 * C::A_BYTES + C::B_BYTES);
-          umma<KIND>(tmem, a0 + koff, blo + koff, idesc, 1u);
-          umma<KIND>(tmem, alo + koff, b0 + koff, idesc, 1u);
+          umma<KIND>(dacc, a0 + koff, blo + koff, idesc, 1u);
+          umma<KIND>(dacc, alo + koff, b0 + koff, idesc, 1u);
         }
       }
       umma_commit(&empty[s]);
@@ -312,11 +331,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const int row = m0 + warp * 32 + lane;
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-  if (sk.splits == 1) {
+  if (in_cta) {
 #pragma unroll 1
     for (int c = 0; c < BN; c += 16) {
       float v[16];
       tmem_ld16(trow + c, v);
+      for (int sg = 1; sg < S; ++sg) {  // segment order 0..S-1
+        float u[16];
+        tmem_ld16(trow + sg * BN + c, u);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] += u[j];
+      }
       if ((dbg & 4) == 0 && row < M && n0 + c < N) epi_store16(e, row, n0 + c, N, v);
     }
   } else {
@@ -334,7 +359,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     }
     cluster_sync_all();
-    const int S = sk.splits, rows = TC_BM / S, r0 = blockIdx.z * rows;
+    const int rows = TC_BM / S, r0 = blockIdx.z * rows;
     const int chunks = rows * (BN / 16);
     for (int idx = threadIdx.x; idx < chunks; idx += TC_THREADS) {
       const int r = r0 + idx / (BN / 16), c = (idx % (BN / 16)) * 16;
@@ -359,7 +384,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   if (warp == 2) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "n"(C::TMEM_COLS));
+                 "r"(tcols));
   }
 }
 

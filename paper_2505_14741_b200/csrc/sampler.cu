@@ -96,10 +96,23 @@ __device__ __forceinline__ void gen_z(uint64_t seed, int t, int64_t i0, double* 
 template <typename T, int VEC, bool S>
 __device__ __forceinline__ void step_vec(Vec<T, VEC, S>& x, const Vec<T, VEC, S>& e, const ps_step& s,
                                          const double* z) {
+  if constexpr (sizeof(T) == 8) {
+    // fp64 state: the reference's float64 arithmetic op for op (bit-exact)
 #pragma unroll
-  for (int k = 0; k < VEC; ++k)
-    x.v[k] = s.noisy ? ddpm_z(x.v[k], e.v[k], s.c, s.sqrt_a, s.sigma, z[k])
-                     : ddpm(x.v[k], e.v[k], s.c, s.sqrt_a);
+    for (int k = 0; k < VEC; ++k)
+      x.v[k] = s.noisy ? ddpm_z(x.v[k], e.v[k], s.c, s.sqrt_a, s.sigma, z[k])
+                       : ddpm(x.v[k], e.v[k], s.c, s.sqrt_a);
+  } else {
+    // fp32 state: the same op order in IEEE fp32 (the fp32 path rounds every
+    // stored state anyway; fp64 division would make the kernel FP64-bound)
+    const float c = (float)s.c, sa = (float)s.sqrt_a, sg = (float)s.sigma;
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) {
+      float m = __fdiv_rn(__fsub_rn((float)x.v[k], __fmul_rn(c, (float)e.v[k])), sa);
+      if (s.noisy) m = __fadd_rn(m, __fmul_rn(sg, (float)z[k]));
+      x.v[k] = m;
+    }
+  }
 }
 
 constexpr int ZCACHE = 7;  // roll steps whose z stays in registers (degree <= 8)
@@ -117,7 +130,7 @@ __global__ void __launch_bounds__(256) cycle_kernel(const __grid_constant__ Cycl
   double z[VEC];
   // issue the first PF eps loads up front (independent 16 B loads in flight:
   // the kernel is HBM-bound at large n and latency-bound otherwise)
-  constexpr int PF = 8;
+  constexpr int PF = 16 / VEC;  // 8 (fp64) / 4 (fp32) prefetched eps vectors
   Vec<T, VEC, SCALAR> ev[PF];
 #pragma unroll
   for (int k = 0; k < PF; ++k)

@@ -154,3 +154,18 @@ def test_dit_run_deterministic_and_graph():
     lanes = E.run_strategy(w, sch, E.RunConfig(steps=20, warmup=2, strategy="parastep", degree=4,
                                                seed=9, data_dim=spec.data_dim))
     assert lanes.bitwise_equal(a)
+
+
+@pytest.mark.parametrize("shape", [(256, 1152, 1152), (256, 384, 1536), (256, 1152, 4608)])
+@pytest.mark.parametrize("precision", [0, 1])
+def test_gemm_split_paths_bitwise(shape, precision):
+    """K segments as a DSMEM cluster (small M) and in one CTA (large M) must
+    give identical bits: this is what keeps forward_batch == forward."""
+    M, N, K = shape
+    g = torch.Generator(device="cuda").manual_seed(7)
+    A = torch.randn((M, K), device="cuda", generator=g)
+    W = torch.randn((K, N), device="cuda", generator=g) / K ** 0.5
+    bias = torch.randn(N, device="cuda", generator=g)
+    c_cluster = _gemm(A, W, bias, precision, 2)
+    c_in_cta = _gemm(A, W, bias, precision, 3)
+    assert torch.equal(c_cluster, c_in_cta)

@@ -14,8 +14,8 @@ lib = _lib.load(require_gpu=True)
 shapes = [(256, 4608, 1152), (256, 1152, 1152), (256, 1152, 4608), (256, 3456, 1152),
           (256, 1536, 384), (256, 384, 384), (256, 384, 1536), (256, 1152, 384),
           (2048, 4608, 1152), (8192, 8192, 8192)]
-dbgs = (0, 1, 2, 3, 7, 8, 32)
-print(f"{'M':>6} {'N':>6} {'K':>6} prec   full  noMMA  noTMA   none nostor  empty nosplit"
+dbgs = (0, 1, 2, 3, 7, 8, 32, 64)
+print(f"{'M':>6} {'N':>6} {'K':>6} prec   full  noMMA  noTMA   none nostor  empty nosplit incta"
       "  TF/s(full)")
 for M, N, K in shapes:
     for prec in (1, 0):

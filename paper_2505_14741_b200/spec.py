@@ -124,6 +124,8 @@ SPECS = {
     # test-sized
     "dit_tiny": DiTSpec("dit_tiny", 4, 1, 8, 8, "CHW", 2, 64, 2, 2, freq_dim=32),
     "dit_tiny_video": DiTSpec("dit_tiny_video", 4, 3, 8, 12, "FHWC", 2, 96, 2, 3, freq_dim=32),
+    # long sequence (1728 tokens): exercises the long-L attention kernel
+    "dit_long_video": DiTSpec("dit_long_video", 4, 3, 48, 48, "FHWC", 2, 64, 1, 2, freq_dim=32),
     # BASELINE.json configs[0..1]: "small random-init DiT", latent 4x32x32
     "dit_s2": DiTSpec("dit_s2", 4, 1, 32, 32, "CHW", 2, 384, 12, 6),
     # configs[2]: DiT-XL/2-shaped

@@ -162,6 +162,15 @@ int ps_gemm_test(const float* A, const float* W, const float* bias, float* C, in
  * GEMM launches on zero operands; dbg bit0 = skip MMA, bit1 = skip TMA. */
 float ps_gemm_probe(int M, int N, int K, int precision, int dbg, int iters);
 
+/* Diagnostic (allocates + synchronises): softmax(Q K^T / sqrt(dh)) V over
+ * qkv fp32 [B*L, 3D] (row m = [q | k | v], heads of dh = D/H contiguous)
+ * into out fp32 [B*L, D], operands rounded to bf16: impl 1 = mma.sync flash
+ * attention, impl 2 = tcgen05/TMEM flash attention (dh = 64). */
+int ps_attn_test(const float* qkv, float* out, int B, int L, int H, int D, int impl,
+                 void* cuda_stream);
+/* Diagnostic: mean device time (us) of `iters` back-to-back attention launches. */
+float ps_attn_probe(int B, int L, int H, int D, int impl, int iters);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,127 @@
+// Host side of the tcgen05 flash attention (attn_fmha.cuh) plus C-ABI
+// diagnostics that run one attention against caller buffers.
+
+#include <cmath>
+#include <mutex>
+
+#include "attn_fmha.cuh"
+#include "attn_mma.cuh"
+
+namespace ps {
+
+int fmha_make_map(CUtensorMap* m, const __nv_bfloat16* qkv_bf16, int rows, int D) {
+  return tc_make_map(m, qkv_bf16, 2, 3 * D, rows, FM_BK);
+}
+
+int fmha_launch(const CUtensorMap& map, const FmhaArgs& a, int H, cudaStream_t st) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(fmha_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FM_SMEM);
+  });
+  cudaError_t e = launch_pdl(fmha_tc_kernel, dim3((a.L + FM_BQ - 1) / FM_BQ, H, a.B),
+                             dim3(FM_THREADS), FM_SMEM, st, map, a);
+  if (e != cudaSuccess) return fail((int)e, std::string("fmha: ") + cudaGetErrorString(e));
+  return check_launch("fmha");
+}
+
+static __global__ void f32_to_bf16_n(const float* in, __nv_bfloat16* out, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = __float2bfloat16_rn(in[i]);
+}
+
+static __global__ void bf16_to_f32_n(const __nv_bfloat16* in, float* out, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = __bfloat162float(in[i]);
+}
+
+// One attention over qkv fp32 [B*L, 3D] (dh = D / H) into out fp32 [B*L, D]:
+// impl 1 = mma.sync flash attention (bf16), impl 2 = tcgen05 FMHA (bf16,
+// dh 64). `iters` > 0: return mean device us of that many back-to-back
+// launches instead (qkv/out may then be null). Allocates; test/probe only.
+static float attn_run(const float* qkv, float* out, int B, int L, int H, int D, int impl,
+                      int iters, cudaStream_t st, int* rc_out) {
+  const int dh = D / H;
+  const int64_t nq = (int64_t)B * L * 3 * D, no = (int64_t)B * L * D;
+  __nv_bfloat16 *qb = nullptr, *ob = nullptr;
+  float* qf = nullptr;
+  int rc = 0;
+  float us = -1.f;
+  if (cudaMalloc(&qb, nq * 2) || cudaMalloc(&ob, no * 2) || cudaMalloc(&qf, nq * 4)) {
+    rc = fail(PS_ECUDA, "attn_run: cudaMalloc");
+  }
+  if (!rc) {
+    if (qkv) {
+      f32_to_bf16_n<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(qkv, qb, nq);
+      // the mma.sync kernel reads fp32 qkv: give it the bf16-rounded values
+      bf16_to_f32_n<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(qb, qf, nq);
+    } else {
+      cudaMemsetAsync(qb, 0, nq * 2, st);
+      cudaMemsetAsync(qf, 0, nq * 4, st);
+    }
+    CUtensorMap map;
+    if (impl == 2) {
+      if (dh != FM_DH) rc = fail(PS_EUNSUP, "tcgen05 attention needs head_dim 64");
+      else rc = fmha_make_map(&map, qb, B * L, D);
+    }
+    FmhaArgs fa{L, D, B, 1.4426950408889634f / sqrtf((float)dh), ob};
+    AttnArgs aa{};
+    aa.qkv = qf;
+    aa.L = L;
+    aa.D = D;
+    aa.H = H;
+    aa.dh = dh;
+    aa.scale = 1.0f / sqrtf((float)dh);
+    aa.out_bf16 = ob;
+    auto go = [&]() -> int {
+      if (impl == 2) return fmha_launch(map, fa, H, st);
+      if (!launch_attn_tc(AM_BF16, aa, B, st)) return fail(PS_EUNSUP, "head_dim unsupported");
+      return check_launch("attn_tc");
+    };
+    if (!rc) rc = go();
+    if (!rc && iters > 0) {
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, st);
+      for (int i = 0; i < iters && !rc; ++i) rc = go();
+      cudaEventRecord(b, st);
+      cudaEventSynchronize(b);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, a, b);
+      us = ms * 1000.f / iters;
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+    }
+    if (!rc && out) bf16_to_f32_n<<<(unsigned)((no + 255) / 256), 256, 0, st>>>(ob, out, no);
+    cudaError_t se = cudaStreamSynchronize(st);
+    if (!rc && se != cudaSuccess) rc = fail((int)se, std::string("attn: ") + cudaGetErrorString(se));
+  }
+  cudaFree(qb);
+  cudaFree(ob);
+  cudaFree(qf);
+  *rc_out = rc;
+  return us;
+}
+
+}  // namespace ps
+
+using namespace ps;
+
+extern "C" {
+
+int ps_attn_test(const float* qkv, float* out, int B, int L, int H, int D, int impl, void* cs) {
+  PS_CHECK_ARG(qkv && out && B >= 1 && L >= 1 && H >= 1 && D % H == 0, "bad attention arguments");
+  PS_CHECK_ARG(impl == 1 || impl == 2, "impl must be 1 (mma.sync) or 2 (tcgen05)");
+  int rc = 0;
+  attn_run(qkv, out, B, L, H, D, impl, 0, as_stream(cs), &rc);
+  return rc;
+}
+
+float ps_attn_probe(int B, int L, int H, int D, int impl, int iters) {
+  if (B < 1 || L < 1 || H < 1 || D % H || iters < 1) return -1.f;
+  int rc = 0;
+  float us = attn_run(nullptr, nullptr, B, L, H, D, impl, iters, 0, &rc);
+  return rc ? -1.f : us;
+}
+
+}  // extern "C"

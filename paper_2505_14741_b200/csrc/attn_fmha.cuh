@@ -1,0 +1,291 @@
+// tcgen05 flash attention for long sequences, bf16 (head_dim 64).
+//
+// softmax(Q K^T / sqrt(dh)) V for one (lane b, head, 128-query tile) per CTA,
+// Q/K/V read by TMA straight out of the QKV GEMM's bf16 output [B*L, 3D]
+// (128-byte swizzled boxes of 128 tokens x 64 dims), scores and the output
+// accumulator in TMEM:
+//
+//   warp 4 (1 thread)  TMA:      Q once, then K_j/V_j into a 3-stage ring
+//   warp 5 (1 thread)  MMA:      S_j = Q K_j^T  (M=128, N=128, K=64; 2 TMEM buffers)
+//                                O  += P_j V_j  (M=128, N=64,  K=128; V MN-major)
+//   warps 0-3          softmax:  thread r owns query row r (TMEM lane r):
+//                                tcgen05.ld S row -> exp2 -> P row (bf16) into
+//                                swizzled smem (the A operand of P V)
+//
+// The MMA warp issues S_{j+1} before waiting for P_j, so the score MMA of the
+// next block runs under the softmax of this one. Online softmax with a lazy
+// rescale: a row's reference max only moves when the block max exceeds it by
+// more than 2^8 (then O's row is rescaled in TMEM, after P_{j-1} V_{j-1} has
+// landed); otherwise p = exp2(s - m_ref) <= 256, exact in fp32 and safe in
+// bf16. The final O / l goes out in the proj GEMM's bf16 operand layout.
+// All reductions run in a fixed order: results do not depend on the grid.
+#pragma once
+
+#include "attn_mma.cuh"
+#include "gemm_tc.cuh"
+
+namespace ps {
+
+constexpr int FM_BQ = 128, FM_BK = 128, FM_DH = 64, FM_STAGES = 3;
+constexpr int FM_THREADS = 192;
+constexpr int FM_TILE = 128 * 128;                 // bytes of one 128 x 64 bf16 tile
+constexpr int FM_Q_OFF = 0;
+constexpr int FM_KV_OFF = FM_TILE;                 // stage s: K at +2s*TILE, V at +(2s+1)*TILE
+constexpr int FM_P_OFF = FM_KV_OFF + 2 * FM_STAGES * FM_TILE;  // 2 buffers x 2 atom columns
+constexpr int FM_BAR_OFF = FM_P_OFF + 4 * FM_TILE;
+constexpr int FM_SMEM = FM_BAR_OFF + 256 + 1024;
+constexpr uint32_t FM_TMEM_COLS = 512;             // S0 [0,128) S1 [128,256) O [256,320)
+
+struct FmhaArgs {
+  int L, D, B;
+  float scale_log2;  // log2(e) / sqrt(dh)
+  __nv_bfloat16* out_bf16;  // [B*L, D], row-major (the proj GEMM's A operand)
+};
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),
+      "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]),
+      "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]),
+      "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]),
+      "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__global__ void __launch_bounds__(FM_THREADS, 1)
+    fmha_tc_kernel(const __grid_constant__ CUtensorMap mapQKV, const __grid_constant__ FmhaArgs p) {
+  extern __shared__ __align__(1024) uint8_t fm_smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(fm_smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + FM_BAR_OFF);
+  uint64_t* q_full = bars;                    // 1
+  uint64_t* kv_full = bars + 1;               // FM_STAGES
+  uint64_t* kv_empty = kv_full + FM_STAGES;   // FM_STAGES
+  uint64_t* s_full = kv_empty + FM_STAGES;    // 2
+  uint64_t* p_full = s_full + 2;              // 2
+  uint64_t* pv_done = p_full + 2;             // 2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q0 = blockIdx.x * FM_BQ, head = blockIdx.y, b = blockIdx.z;
+  const int L = p.L;
+  const int nkb = (L + FM_BK - 1) / FM_BK;
+  const int row_base = b * L;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&mapQKV);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < FM_STAGES; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 128);
+      mbar_init(&pv_done[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(FM_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS[2] = {tmem, tmem + 128};
+  const uint32_t tO = tmem + 256;
+  pdl_wait_and_release();
+
+  if (warp == 4) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      mbar_expect_tx(q_full, FM_TILE);
+      tma_load_2d(smem + FM_Q_OFF, &mapQKV, q_full, head * FM_DH, row_base + q0);
+      for (int j = 0; j < nkb; ++j) {
+        const int s = j % FM_STAGES;
+        mbar_wait(&kv_empty[s], ((j / FM_STAGES) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[s], 2 * FM_TILE);
+        uint8_t* st = smem + FM_KV_OFF + 2 * s * FM_TILE;
+        tma_load_2d(st, &mapQKV, &kv_full[s], p.D + head * FM_DH, row_base + j * FM_BK);
+        tma_load_2d(st + FM_TILE, &mapQKV, &kv_full[s], 2 * p.D + head * FM_DH,
+                    row_base + j * FM_BK);
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      constexpr uint32_t idS = make_idesc(KIND_BF16, 128, 128);
+      constexpr uint32_t idPV = make_idesc(KIND_BF16, 128, FM_DH) | (1u << 16);  // B (V) MN-major
+      const uint64_t qd = smem_desc_sw128(smem + FM_Q_OFF);
+      auto issue_s = [&](int j) {
+        const int s = j % FM_STAGES;
+        mbar_wait(&kv_full[s], (j / FM_STAGES) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint64_t kd = smem_desc_sw128(smem + FM_KV_OFF + 2 * s * FM_TILE);
+#pragma unroll
+        for (int k = 0; k < FM_DH / 16; ++k)  // +32 B along K inside the swizzle atom
+          umma<KIND_BF16>(tS[j & 1], qd + 2 * k, kd + 2 * k, idS, k > 0 ? 1u : 0u);
+        umma_commit(&s_full[j & 1]);
+      };
+      mbar_wait(q_full, 0);
+      issue_s(0);
+      if (nkb > 1) issue_s(1);
+      for (int j = 0; j < nkb; ++j) {
+        mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int s = j % FM_STAGES;
+        const uint8_t* pb = smem + FM_P_OFF + (j & 1) * 2 * FM_TILE;
+        const uint64_t vd = smem_desc_sw128(smem + FM_KV_OFF + (2 * s + 1) * FM_TILE);
+#pragma unroll
+        for (int k = 0; k < FM_BK / 16; ++k) {
+          // P: K-major, keys [64a, 64a+64) in atom column a; V: MN-major, 16 keys = 2048 B
+          const uint64_t pd = smem_desc_sw128(pb + (k >> 2) * FM_TILE) + 2 * (k & 3);
+          umma<KIND_BF16>(tO, pd, vd + (uint64_t)(k * 2048 >> 4), idPV, (j | k) ? 1u : 0u);
+        }
+        umma_commit(&kv_empty[s]);
+        umma_commit(&pv_done[j & 1]);
+        if (j + 2 < nkb) issue_s(j + 2);
+      }
+    }
+  } else {
+    // ---------------- softmax warps: thread r <-> query row r <-> TMEM lane r
+    const int r = threadIdx.x;  // 0..127
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    const float sl2 = p.scale_log2;
+    float m_ref = -INFINITY, l = 0.f;
+    for (int j = 0; j < nkb; ++j) {
+      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      float s[FM_BK];
+#pragma unroll
+      for (int c = 0; c < FM_BK / 32; ++c) tmem_ld32(tS[j & 1] + lane_off + c * 32, s + c * 32);
+      tmem_ld_wait();
+      const int valid = L - j * FM_BK;  // keys of this block inside the lane
+      if (valid < FM_BK) {
+#pragma unroll
+        for (int c = 0; c < FM_BK; ++c)
+          if (c >= valid) s[c] = -INFINITY;
+      }
+      float mx = s[0];
+#pragma unroll
+      for (int c = 1; c < FM_BK; ++c) mx = fmaxf(mx, s[c]);
+      const float m_new = mx * sl2;
+      if (j == 0) {
+        m_ref = m_new;
+      } else {
+        const bool need = m_new > m_ref + 8.f;
+        if (__any_sync(0xffffffffu, need)) {
+          // O's row must hold P_{j-1} V_{j-1} before it is rescaled
+          mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const float m_tgt = need ? m_new : m_ref;
+          const float f = fast_exp2(m_ref - m_tgt);
+          l *= f;
+          m_ref = m_tgt;
+#pragma unroll
+          for (int c = 0; c < FM_DH / 32; ++c) {
+            float o[32];
+            tmem_ld32(tO + lane_off + c * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] *= f;
+            tmem_st32(tO + lane_off + c * 32, o);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+      }
+      // P buffer (j & 1) was last read by P_{j-2} V_{j-2}
+      if (j >= 2) mbar_wait(&pv_done[j & 1], ((j - 2) >> 1) & 1);
+      uint8_t* prow = smem + FM_P_OFF + (j & 1) * 2 * FM_TILE + r * 128;
+      float rs = 0.f;
+#pragma unroll
+      for (int kc = 0; kc < FM_BK / 8; ++kc) {  // 16-byte chunks of 8 keys
+        uint32_t u[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float p0 = fast_exp2(fmaf(s[kc * 8 + 2 * q], sl2, -m_ref));
+          const float p1 = fast_exp2(fmaf(s[kc * 8 + 2 * q + 1], sl2, -m_ref));
+          rs += p0 + p1;
+          u[q] = pack_bf16(p0, p1);
+        }
+        const int a = kc >> 3, c = kc & 7;
+        *reinterpret_cast<uint4*>(prow + a * FM_TILE + ((c ^ (r & 7)) << 4)) =
+            make_uint4(u[0], u[1], u[2], u[3]);
+      }
+      l += rs;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&p_full[j & 1]);
+    }
+    // ---------------- epilogue: O / l -> bf16 [B*L, D]
+    mbar_wait(&pv_done[(nkb - 1) & 1], ((nkb - 1) >> 1) & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const float inv = 1.f / l;
+    const bool ok = q0 + r < L;
+    __nv_bfloat16* orow = p.out_bf16 + (int64_t)(row_base + q0 + r) * p.D + head * FM_DH;
+#pragma unroll
+    for (int c = 0; c < FM_DH / 32; ++c) {
+      float o[32];
+      tmem_ld32(tO + lane_off + c * 32, o);
+      tmem_ld_wait();
+      if (ok) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 u;
+          u.x = pack_bf16(o[8 * q] * inv, o[8 * q + 1] * inv);
+          u.y = pack_bf16(o[8 * q + 2] * inv, o[8 * q + 3] * inv);
+          u.z = pack_bf16(o[8 * q + 4] * inv, o[8 * q + 5] * inv);
+          u.w = pack_bf16(o[8 * q + 6] * inv, o[8 * q + 7] * inv);
+          *reinterpret_cast<uint4*>(orow + c * 32 + 8 * q) = u;
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(FM_TMEM_COLS));
+  }
+}
+
+// qkv_bf16: [rows, 3D] row-major; the map's box is 64 dims x 128 tokens
+int fmha_make_map(CUtensorMap* m, const __nv_bfloat16* qkv_bf16, int rows, int D);
+int fmha_launch(const CUtensorMap& map, const FmhaArgs& a, int H, cudaStream_t st);
+
+}  // namespace ps

@@ -13,7 +13,7 @@ enum EpiMode { EPI_STORE = 0, EPI_GELU = 1, EPI_RESID = 2, EPI_UNPATCH = 3 };
 struct Epi {
   int mode;
   const float* bias;
-  // EPI_STORE: out[M, N] fp32; EPI_GELU: act formats
+  // EPI_STORE: out[M, N] fp32 and/or out_bf16; EPI_GELU: act formats
   float* out;
   __nv_bfloat16* out_bf16;
   float* out_hi;
@@ -34,7 +34,8 @@ __device__ __forceinline__ void epi_store(const Epi& e, int m, int n, int N, flo
   const int64_t idx = (int64_t)m * N + n;
   switch (e.mode) {
     case EPI_STORE:
-      e.out[idx] = v;
+      if (e.out) e.out[idx] = v;
+      if (e.out_bf16) e.out_bf16[idx] = __float2bfloat16_rn(v);
       break;
     case EPI_GELU: {
       const float g = gelu_tanh_f(v);
@@ -82,10 +83,21 @@ __device__ __forceinline__ void epi_store16(const Epi& e, int m, int n, int N, c
     x[4 * q + 3] = v[4 * q + 3] + bb.w;
   }
   if (e.mode == EPI_STORE) {
+    if (e.out)
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      *reinterpret_cast<float4*>(e.out + base + 4 * q) =
-          make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+      for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<float4*>(e.out + base + 4 * q) =
+            make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+    if (e.out_bf16) {  // bf16 copy (the tcgen05 attention's Q/K/V operand)
+      uint32_t u[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(x[2 * q], x[2 * q + 1]);
+        u[q] = *reinterpret_cast<uint32_t*>(&h2);
+      }
+      *reinterpret_cast<uint4*>(e.out_bf16 + base) = make_uint4(u[0], u[1], u[2], u[3]);
+      *reinterpret_cast<uint4*>(e.out_bf16 + base + 8) = make_uint4(u[4], u[5], u[6], u[7]);
+    }
   } else if (e.mode == EPI_GELU) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) x[j] = gelu_tanh_f(x[j]);

@@ -23,7 +23,7 @@ static int get_encode() {
 }
 
 // 2-D K-major map: dims {K, rows}, box {128 B of K, box_rows}, 128 B swizzle
-static int make_map(CUtensorMap* m, const void* base, int esz, int K, int rows, int box_rows) {
+int tc_make_map(CUtensorMap* m, const void* base, int esz, int K, int rows, int box_rows) {
   if (int rc = get_encode()) return rc;
   CUtensorMapDataType dt =
       esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
@@ -73,7 +73,7 @@ static int alloc_operand(TcActs& acts, TcOperand& op, int rows, int cols, int pr
     if (e != cudaSuccess) return fail((int)e, "cudaMalloc operand");
     acts.owned.push_back(op.bf16);
     cudaMemset(op.bf16, 0, n * 2);
-    return make_map(&op.map_main, op.bf16, 2, cols, rows, TC_BM);
+    return tc_make_map(&op.map_main, op.bf16, 2, cols, rows, TC_BM);
   }
   e = cudaMalloc(&op.hi, n * 4);
   if (e == cudaSuccess) {
@@ -84,8 +84,8 @@ static int alloc_operand(TcActs& acts, TcOperand& op, int rows, int cols, int pr
   acts.owned.push_back(op.lo);
   cudaMemset(op.hi, 0, n * 4);
   cudaMemset(op.lo, 0, n * 4);
-  if (int rc = make_map(&op.map_main, op.hi, 4, cols, rows, TC_BM)) return rc;
-  return make_map(&op.map_lo, op.lo, 4, cols, rows, TC_BM);
+  if (int rc = tc_make_map(&op.map_main, op.hi, 4, cols, rows, TC_BM)) return rc;
+  return tc_make_map(&op.map_lo, op.lo, 4, cols, rows, TC_BM);
 }
 
 static int g_dbg = 0;  // ps_gemm_probe only
@@ -189,10 +189,10 @@ int tc_prepare(TcWeights& w, TcActs& acts, const std::vector<const float*>& Ws,
     const int boxes[3] = {32, 64, 128};
     for (int bi = 0; bi < 3; ++bi) {
       if (precision == 1) {
-        if (int rc = make_map(&L.map_b[bi], L.w_main, 2, L.K, L.N, boxes[bi])) return rc;
+        if (int rc = tc_make_map(&L.map_b[bi], L.w_main, 2, L.K, L.N, boxes[bi])) return rc;
       } else if (bi < 2) {
-        if (int rc = make_map(&L.map_b[bi], L.w_main, 4, L.K, L.N, boxes[bi])) return rc;
-        if (int rc = make_map(&L.map_blo[bi], L.w_lo, 4, L.K, L.N, boxes[bi])) return rc;
+        if (int rc = tc_make_map(&L.map_b[bi], L.w_main, 4, L.K, L.N, boxes[bi])) return rc;
+        if (int rc = tc_make_map(&L.map_blo[bi], L.w_lo, 4, L.K, L.N, boxes[bi])) return rc;
       }
     }
   }

@@ -395,5 +395,7 @@ int tc_prepare(TcWeights& w, TcActs& acts, const std::vector<const float*>& Ws,
 int tc_gemm(const TcWeights& w, int layer, const TcOperand& A, int M, int N, int K, const Epi& e,
             int precision, cudaStream_t st);
 void tc_release(TcWeights& w, TcActs& acts);
+// 2-D K-major TMA map: dims {K, rows}, box {128 B of K, box_rows}, 128 B swizzle
+int tc_make_map(CUtensorMap* m, const void* base, int esz, int K, int rows, int box_rows);
 // standalone test entry (C-ABI wrapper in gemm_tc.cu)
 }  // namespace ps

@@ -8,8 +8,9 @@
 // fp32), the same flatten order as the reference's numpy vector, so the RNG
 // counter of element i is i. A thread owns VEC consecutive elements (16 B:
 // 2 x fp64 or 4 x fp32) = 1 or 2 Box-Muller pairs, so both normals of a pair
-// are produced by one log/sqrt/sincos. The per-element chain is kept in fp64
-// registers for the whole launch (apply steps, then each lane's roll), so
+// are produced by one log/sqrt/sincos. The per-element chain is kept in
+// registers for the whole launch (apply steps, then each lane's roll; fp64
+// for the fp64 state, fp32 for the DiT's fp32 state), so
 // one launch reads x + c eps (+ lane caches) and writes x + lanes: the
 // minimum traffic for the round.
 
@@ -46,6 +47,11 @@ struct CycleParams {
   void* rec[PS_MAX_CYCLE];
   const void* cache[PS_MAX_CYCLE];
   void* lane_out[PS_MAX_CYCLE];
+  // fp32-state copies of apply/roll, rounded on the host (see cycle_f32_kernel)
+  struct F32 {
+    float c, inv_sa, sigma;
+    int noisy;
+  } fa[PS_MAX_CYCLE], fr[PS_MAX_CYCLE];
 };
 
 template <typename T, int VEC, bool SCALAR = false>
@@ -169,6 +175,132 @@ __global__ void __launch_bounds__(256) cycle_kernel(const __grid_constant__ Cycl
   }
 }
 
+// ---------------------------------------------------------------------------
+// fp32 state (the DiT predictors): the chain lives in fp32 registers, one
+// float4 (16 B) per thread, and every eps vector of the round is loaded up
+// front so 1 + c independent 16-B loads are in flight per thread (the kernel
+// is a pure HBM stream at large n). The division by sqrt(alpha_t) becomes a
+// multiplication by the host-rounded reciprocal: every op rounds explicitly
+// (no contraction), so apply and roll chains are bit-identical wherever they
+// compute the same step, and the fp32 path stays well inside its 1e-4 bound.
+using F32Step = CycleParams::F32;
+
+static F32Step f32_step_host(const ps_step& s) {
+  return F32Step{(float)s.c, (float)(1.0 / s.sqrt_a), (float)s.sigma, s.noisy};
+}
+
+__device__ __forceinline__ float f32_ddpm(float x, float e, const F32Step& s, float z) {
+  float m = __fmul_rn(__fsub_rn(x, __fmul_rn(s.c, e)), s.inv_sa);
+  return s.noisy ? __fadd_rn(m, __fmul_rn(s.sigma, z)) : m;
+}
+
+template <bool AL>
+__device__ __forceinline__ float4 f32_ld4(const void* base, int64_t i0, int cnt) {
+  const float* p = reinterpret_cast<const float*>(base) + i0;
+  if (AL && cnt == 4) return __ldg(reinterpret_cast<const float4*>(p));
+  float v[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) v[k] = k < cnt ? __ldg(p + k) : 0.f;
+  return make_float4(v[0], v[1], v[2], v[3]);
+}
+
+template <bool AL>
+__device__ __forceinline__ void f32_st4(void* base, int64_t i0, int cnt, float4 v) {
+  float* p = reinterpret_cast<float*>(base) + i0;
+  if (AL && cnt == 4) {
+    *reinterpret_cast<float4*>(p) = v;
+    return;
+  }
+  const float a[4] = {v.x, v.y, v.z, v.w};
+  for (int k = 0; k < cnt; ++k) p[k] = a[k];
+}
+
+__device__ __forceinline__ void f32_step4(float4& x, const float4& e, const F32Step& s,
+                                          const float* z) {
+  x.x = f32_ddpm(x.x, e.x, s, z[0]);
+  x.y = f32_ddpm(x.y, e.y, s, z[1]);
+  x.z = f32_ddpm(x.z, e.z, s, z[2]);
+  x.w = f32_ddpm(x.w, e.w, s, z[3]);
+}
+
+__device__ __forceinline__ void f32_gen_z(uint64_t seed, const ps_step& s, int64_t i0, float* z) {
+  if (!s.noisy) {
+    z[0] = z[1] = z[2] = z[3] = 0.f;
+    return;
+  }
+  double d[4];
+  gen_z<4>(seed, s.t, i0, d);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) z[k] = (float)d[k];
+}
+
+constexpr int F32_PF = 8;  // eps vectors loaded up front (c <= 8 covers degree <= 8)
+
+// NOISY = some step of this launch adds sigma*z (posterior mode). In zero
+// mode ("DDIM") no z is generated and the lane caches are loaded up front
+// too; with z the per-lane caches are loaded one at a time instead, so the
+// z registers of the roll steps fit.
+template <bool AL, bool NOISY>
+__global__ void __launch_bounds__(256, NOISY ? 2 : 4) cycle_f32_kernel(const __grid_constant__ CycleParams p) {
+  pdl_wait_and_release();
+  const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (i0 >= p.n) return;
+  const int cnt = (p.n - i0) < 4 ? (int)(p.n - i0) : 4;
+
+  float4 x = f32_ld4<AL>(p.x_in, i0, cnt);
+  float4 ev[F32_PF];
+#pragma unroll
+  for (int k = 0; k < F32_PF; ++k)
+    if (k < p.n_apply) ev[k] = f32_ld4<AL>(p.eps[k], i0, cnt);
+  float z[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int k = 0; k < PS_MAX_CYCLE; ++k) {
+    if (k >= p.n_apply) break;
+    if (p.rec[k]) f32_st4<AL>(p.rec[k], i0, cnt, x);
+    const float4 e = k < F32_PF ? ev[k] : f32_ld4<AL>(p.eps[k], i0, cnt);
+    if (NOISY) f32_gen_z(*p.seed, p.apply[k], i0, z);
+    f32_step4(x, e, p.fa[k], z);
+  }
+  if (p.n_apply > 0) f32_st4<AL>(p.x_out, i0, cnt, x);
+  if (p.lane_hi <= 1) return;
+
+  const int jlo = max(p.lane_lo, 1);
+  if constexpr (!NOISY) {
+    float4 cv[F32_PF];
+#pragma unroll
+    for (int j = 1; j < F32_PF; ++j)
+      if (j >= jlo && j < p.lane_hi) cv[j] = f32_ld4<AL>(p.cache[j], i0, cnt);
+#pragma unroll
+    for (int j = 1; j < PS_MAX_CYCLE; ++j) {
+      if (j >= p.lane_hi) break;
+      if (j < jlo) continue;
+      const float4 c = j < F32_PF ? cv[j] : f32_ld4<AL>(p.cache[j], i0, cnt);
+      float4 xj = x;
+      for (int k = 0; k < j; ++k) f32_step4(xj, c, p.fr[k], z);
+      f32_st4<AL>(p.lane_out[j], i0, cnt, xj);
+    }
+  } else {
+    const uint64_t seed = *p.seed;
+    const int nz = p.lane_hi - 1;  // lane j needs roll steps 0..j-1
+    float zc[ZCACHE][4];
+#pragma unroll
+    for (int k = 0; k < ZCACHE; ++k)
+      if (k < nz) f32_gen_z(seed, p.roll[k], i0, zc[k]);
+    for (int j = jlo; j < p.lane_hi; ++j) {
+      const float4 c = f32_ld4<AL>(p.cache[j], i0, cnt);
+      float4 xj = x;
+#pragma unroll
+      for (int k = 0; k < ZCACHE; ++k)
+        if (k < j) f32_step4(xj, c, p.fr[k], zc[k]);
+      for (int k = ZCACHE; k < j; ++k) {
+        f32_gen_z(seed, p.roll[k], i0, z);
+        f32_step4(xj, c, p.fr[k], z);
+      }
+      f32_st4<AL>(p.lane_out[j], i0, cnt, xj);
+    }
+  }
+}
+
 template <typename T>
 __global__ void step_z_kernel(const T* x, const T* e, const T* z, T* out, int64_t n, ps_step s) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -210,6 +342,24 @@ template <typename T>
 static int launch_cycle(const CycleParams& p, cudaStream_t st, bool vec_ok) {
   constexpr int VEC = 16 / sizeof(T);
   cudaError_t e;
+  if constexpr (sizeof(T) == 4) {
+    // fp32 state: one float4 per thread (scalar accesses when unaligned)
+    const int64_t threads = (p.n + 3) / 4;
+    const int bs = threads >= 148 * 512 ? 256 : 64;
+    const unsigned blocks = (unsigned)((threads + bs - 1) / bs);
+    bool noisy = false;
+    for (int k = 0; k < p.n_apply; ++k) noisy |= p.apply[k].noisy != 0;
+    for (int k = 0; k + 1 < p.lane_hi; ++k) noisy |= p.roll[k].noisy != 0;
+    const dim3 g(blocks), b(bs);
+    if (vec_ok)
+      e = noisy ? launch_pdl(cycle_f32_kernel<true, true>, g, b, 0, st, p)
+                : launch_pdl(cycle_f32_kernel<true, false>, g, b, 0, st, p);
+    else
+      e = noisy ? launch_pdl(cycle_f32_kernel<false, true>, g, b, 0, st, p)
+                : launch_pdl(cycle_f32_kernel<false, false>, g, b, 0, st, p);
+    if (e != cudaSuccess) return fail((int)e, std::string("cycle_f32: ") + cudaGetErrorString(e));
+    return check_launch("cycle_f32");
+  } else {
   // small latents (e.g. 4096 elements): 64-thread blocks spread over more SMs
   if (vec_ok) {
     int64_t threads = (p.n + VEC - 1) / VEC;
@@ -225,6 +375,7 @@ static int launch_cycle(const CycleParams& p, cudaStream_t st, bool vec_ok) {
   }
   if (e != cudaSuccess) return fail((int)e, std::string("cycle_kernel: ") + cudaGetErrorString(e));
   return check_launch("cycle_kernel");
+  }
 }
 
 }  // namespace ps
@@ -320,13 +471,17 @@ int ps_sched_cycle(const void* x_in, void* x_out, int64_t n, int dtype, const ui
   bool vec_ok = ((uintptr_t)x_in % 16 == 0) && ((uintptr_t)x_out % 16 == 0);
   for (int k = 0; k < n_apply; ++k) {
     p.apply[k] = host_apply[k];
+    p.fa[k] = f32_step_host(host_apply[k]);
     p.eps[k] = host_eps_apply[k];
     PS_CHECK_ARG(p.eps[k] != nullptr, "null eps pointer");
     p.rec[k] = host_rec_x ? host_rec_x[k] : nullptr;
     vec_ok = vec_ok && ((uintptr_t)p.eps[k] % 16 == 0) && ((uintptr_t)p.rec[k] % 16 == 0);
   }
   if (lane_hi > 1) {
-    for (int k = 0; k < lane_hi - 1; ++k) p.roll[k] = host_roll[k];
+    for (int k = 0; k < lane_hi - 1; ++k) {
+      p.roll[k] = host_roll[k];
+      p.fr[k] = f32_step_host(host_roll[k]);
+    }
     for (int j = (lane_lo > 1 ? lane_lo : 1); j < lane_hi; ++j) {
       p.cache[j] = host_lane_cache[j];
       p.lane_out[j] = host_lane_out[j];

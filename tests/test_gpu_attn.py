@@ -1,0 +1,87 @@
+"""GPU parity of the attention kernels against a plain PyTorch fp32 reference.
+
+Both kernels run on bf16-rounded Q/K/V (the bf16 predictor path) and round
+P to bf16 before P V, so the reference is softmax(QK^T/sqrt(dh))V in fp32
+on the same bf16-rounded inputs; tolerance: max |err| <= 2e-2 * max |ref|
+and mean |err| <= 4e-3 * mean |ref| (bf16 has an 8-bit mantissa).
+"""
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2505_14741_b200 import _lib  # noqa: E402
+
+
+def _attn(qkv, B, L, H, D, impl):
+    lib = _lib.load(require_gpu=True)
+    out = torch.full((B * L, D), float("nan"), dtype=torch.float32, device="cuda")
+    _lib.check(lib.ps_attn_test(_lib.ptr(qkv), _lib.ptr(out), B, L, H, D, impl,
+                                _lib.stream_ptr()), "attn_test")
+    torch.cuda.synchronize()
+    return out
+
+
+def _ref(qkv, B, L, H, D):
+    dh = D // H
+    x = qkv.to(torch.bfloat16).float().view(B, L, 3, H, dh)
+    q, k, v = (x[:, :, i].permute(0, 2, 1, 3) for i in range(3))  # B H L dh
+    o = torch.nn.functional.scaled_dot_product_attention(q, k, v)
+    return o.permute(0, 2, 1, 3).reshape(B * L, D)
+
+
+def _check(got, ref):
+    err = (got - ref).abs()
+    assert torch.isfinite(got).all()
+    assert err.max().item() <= 2e-2 * ref.abs().max().item(), err.max().item()
+    assert err.mean().item() <= 4e-3 * ref.abs().mean().item(), err.mean().item()
+
+
+# L: exact multiples of the 128-key block, ragged tails (1 and 127 extra keys),
+# a sequence shorter than one block, and two lanes whose blocks straddle the
+# lane boundary
+@pytest.mark.parametrize("B,L,H", [(1, 128, 1), (1, 256, 2), (2, 1000, 2), (1, 129, 3),
+                                   (3, 383, 2), (1, 77, 1), (2, 2048, 4)])
+@pytest.mark.parametrize("impl", [1, 2])
+def test_attention_vs_torch(B, L, H, impl):
+    D = 64 * H
+    g = torch.Generator(device="cuda").manual_seed(B * 1000 + L * 7 + H)
+    qkv = torch.randn((B * L, 3 * D), device="cuda", generator=g)
+    _check(_attn(qkv, B, L, H, D, impl), _ref(qkv, B, L, H, D))
+
+
+def test_attention_peaked_scores_rescale():
+    """Large, drifting logits force the lazy O rescale (max jumps > 2^8)."""
+    B, L, H = 1, 1536, 2
+    D = 64 * H
+    g = torch.Generator(device="cuda").manual_seed(5)
+    qkv = torch.randn((B * L, 3 * D), device="cuda", generator=g)
+    ramp = torch.linspace(0.0, 6.0, L, device="cuda")[:, None]
+    qkv[:, :D] *= 4.0
+    qkv[:, D:2 * D] *= 4.0 * (1.0 + ramp)  # later keys dominate -> the max keeps growing
+    got = _attn(qkv, B, L, H, D, 2)
+    _check(got, _ref(qkv, B, L, H, D))
+
+
+def test_attention_long_cogvideox_head():
+    """One CogVideoX-shaped head: 17,550 tokens (137 full key blocks + 14)."""
+    B, L, H = 1, 17550, 1
+    D = 64
+    g = torch.Generator(device="cuda").manual_seed(11)
+    qkv = torch.randn((B * L, 3 * D), device="cuda", generator=g)
+    got = _attn(qkv, B, L, H, D, 2)
+    _check(got, _ref(qkv, B, L, H, D))
+
+
+def test_attention_tc_matches_mma_path():
+    B, L, H = 2, 700, 3
+    D = 64 * H
+    g = torch.Generator(device="cuda").manual_seed(3)
+    qkv = torch.randn((B * L, 3 * D), device="cuda", generator=g)
+    a = _attn(qkv, B, L, H, D, 1)
+    b = _attn(qkv, B, L, H, D, 2)
+    assert (a - b).abs().max().item() <= 2e-2 * a.abs().max().item()

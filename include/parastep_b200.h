@@ -162,6 +162,46 @@ int ps_gemm_test(const float* A, const float* W, const float* bias, float* C, in
  * GEMM launches on zero operands; dbg bit0 = skip MMA, bit1 = skip TMA. */
 float ps_gemm_probe(int M, int N, int K, int precision, int dbg, int iters);
 
+/* ---- U-Net-shaped predictor (paper_2505_14741_b200/unet_spec.py) -------
+ * A native executor for the op list unet_spec.plan() emits (bf16 tcgen05
+ * GEMMs: convolutions as implicit im2col GEMMs with GroupNorm+SiLU, concat
+ * and resampling fused into the operand gather; tcgen05 attention). */
+typedef struct ps_unet_op {
+  int32_t kind;        /* 0 conv (im2col GEMM), 1 linear (token GEMM), 2 attention */
+  int32_t layer;       /* weight index, -1 none */
+  int32_t pre;         /* A producer: 0 none (in1 is bf16 already), 1 convert, 2 GN, 3 GN+SiLU, 4 LN */
+  int32_t in1, in2;    /* buffer ids (-2 = the forward's latent x, CHW); in2 -1 unless concat */
+  int32_t c1, c2;      /* channels of in1 / in2 */
+  int32_t h, w;        /* input spatial size */
+  int32_t taps;        /* 9 (3x3, pad 1) or 1 */
+  int32_t resample;    /* 0 none, 1 stride-2, 2 nearest-2x before the conv */
+  int32_t cout;
+  int32_t temb_layer;  /* ResBlock time projection layer, -1 none */
+  int32_t temb_off;    /* its column offset in the concatenated time table */
+  int32_t resid;       /* fp32 buffer added in the epilogue, -1 none */
+  int32_t out;         /* output buffer id (-3 = eps, CHW scatter) */
+  int32_t out_bf16;    /* output buffer is bf16 */
+  int32_t act;         /* 1 = GELU-tanh epilogue */
+  int32_t heads;       /* attention heads (head_dim 64) */
+  float eps;           /* GN / LN epsilon */
+} ps_unet_op;
+
+typedef struct ps_unet_config {
+  int32_t in_channels, height, width, groups, freq_dim, temb_dim, temb_cols, max_batch;
+  int32_t n_ops, n_bufs;
+  const ps_unet_op* ops;
+  void* const* bufs;   /* device buffers sized for max_batch, owned by the caller */
+} ps_unet_config;
+
+typedef struct ps_unet ps_unet;
+/* weights: W[i], b[i] in unet_spec.layer_table order; freq_table rows t =
+ * time_embed(t, freq_dim); pos unused */
+int ps_unet_create(const ps_unet_config* cfg, const ps_dit_weights* w, ps_unet** out);
+int ps_unet_forward(ps_unet* h, const float* x, const int32_t* host_ts, int B, float* eps_out,
+                    void* cuda_stream);
+int ps_unet_destroy(ps_unet* h);
+int ps_unet_kernels_per_forward(const ps_unet* h);
+
 /* Diagnostic (allocates + synchronises): softmax(Q K^T / sqrt(dh)) V over
  * qkv fp32 [B*L, 3D] (row m = [q | k | v], heads of dh = D/H contiguous)
  * into out fp32 [B*L, D], operands rounded to bf16: impl 1 = mma.sync flash

@@ -21,12 +21,13 @@
 // All reductions run in a fixed order: results do not depend on the grid.
 #pragma once
 
+#include "attn_fmha.h"
 #include "attn_mma.cuh"
 #include "gemm_tc.cuh"
 
 namespace ps {
 
-constexpr int FM_BQ = 128, FM_BK = 128, FM_DH = 64, FM_STAGES = 3;
+constexpr int FM_BQ = 128, FM_BK = 128, FM_DH = FM_HEAD_DIM, FM_STAGES = 3;
 constexpr int FM_THREADS = 192;
 constexpr int FM_TILE = 128 * 128;                 // bytes of one 128 x 64 bf16 tile
 constexpr int FM_Q_OFF = 0;
@@ -35,12 +36,6 @@ constexpr int FM_P_OFF = FM_KV_OFF + 2 * FM_STAGES * FM_TILE;  // 2 buffers x 2 
 constexpr int FM_BAR_OFF = FM_P_OFF + 4 * FM_TILE;
 constexpr int FM_SMEM = FM_BAR_OFF + 256 + 1024;
 constexpr uint32_t FM_TMEM_COLS = 512;             // S0 [0,128) S1 [128,256) O [256,320)
-
-struct FmhaArgs {
-  int L, D, B;
-  float scale_log2;  // log2(e) / sqrt(dh)
-  __nv_bfloat16* out_bf16;  // [B*L, D], row-major (the proj GEMM's A operand)
-};
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   uint32_t r[32];
@@ -283,9 +278,5 @@ __global__ void __launch_bounds__(FM_THREADS, 1)
                  "r"(FM_TMEM_COLS));
   }
 }
-
-// qkv_bf16: [rows, 3D] row-major; the map's box is 64 dims x 128 tokens
-int fmha_make_map(CUtensorMap* m, const __nv_bfloat16* qkv_bf16, int rows, int D);
-int fmha_launch(const CUtensorMap& map, const FmhaArgs& a, int H, cudaStream_t st);
 
 }  // namespace ps

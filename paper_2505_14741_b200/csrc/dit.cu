@@ -10,6 +10,7 @@
 #include "gemm_simt.cuh"
 #include "gemm_tc.cuh"
 #include "attn_mma.cuh"
+#include "attn_fmha.h"
 
 using namespace ps;
 
@@ -41,6 +42,10 @@ struct ps_dit {
   TcWeights tcw;
   TcActs tca;
   bool use_tc;
+  // bf16 path, head_dim 64: QKV GEMM writes bf16 Q/K/V, tcgen05 attention
+  bool use_fmha = false;
+  __nv_bfloat16* qkv_bf16 = nullptr;
+  CUtensorMap qkv_map;
   double flops;
 };
 
@@ -54,50 +59,6 @@ static int dalloc(ps_dit* h, void** p, size_t bytes) {
 template <typename T>
 static int dalloc_t(ps_dit* h, T** p, size_t count) {
   return dalloc(h, reinterpret_cast<void**>(p), count * sizeof(T) + 256);
-}
-
-template <typename TW, int MAXB>
-static void gemv_launch(const GemvArgs& p, cudaStream_t st) {
-  constexpr int C = GvLoad<TW>::C;
-  const size_t smem = gemv_smem<TW>(p.B, p.K);
-  launch_pdl(gemv_kernel<TW, MAXB>, dim3((p.N + 32 * C - 1) / (32 * C)), dim3(GV_WARPS * 32), smem,
-             st, p);
-}
-
-template <typename TW>
-static void gemv_set_attr() {
-  cudaFuncSetAttribute(gemv_kernel<TW, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
-  cudaFuncSetAttribute(gemv_kernel<TW, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
-  cudaFuncSetAttribute(gemv_kernel<TW, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
-  cudaFuncSetAttribute(gemv_kernel<TW, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
-}
-
-// W is fp32 or bf16 (wbf16), (K, N) row-major, N % (4|8) == 0
-static int gemv(const float* in, int64_t in_stride, const int32_t* rows, const void* W, bool wbf16,
-                const float* bias, float* out, int K, int N, int B, int act, cudaStream_t st) {
-  GemvArgs p{};
-  p.in = in;
-  p.in_stride = in_stride;
-  for (int b = 0; b < B; ++b) p.in_row[b] = rows ? rows[b] : b;
-  p.W = W;
-  p.bias = bias;
-  p.out = out;
-  p.K = K;
-  p.N = N;
-  p.B = B;
-  p.act = act;
-  if (wbf16) {
-    if (B <= 1) gemv_launch<__nv_bfloat16, 1>(p, st);
-    else if (B <= 4) gemv_launch<__nv_bfloat16, 4>(p, st);
-    else if (B <= 8) gemv_launch<__nv_bfloat16, 8>(p, st);
-    else gemv_launch<__nv_bfloat16, 16>(p, st);
-  } else {
-    if (B <= 1) gemv_launch<float, 1>(p, st);
-    else if (B <= 4) gemv_launch<float, 4>(p, st);
-    else if (B <= 8) gemv_launch<float, 8>(p, st);
-    else gemv_launch<float, 16>(p, st);
-  }
-  return check_launch("gemv");
 }
 
 static int ln_mod(ps_dit* h, int rows, int shift_off, int scale_off, const TcOperand* dst,
@@ -248,6 +209,14 @@ int ps_dit_create(const ps_dit_config* cfg, const ps_dit_weights* w, ps_dit** ou
       return rc;
     }
   }
+  if (h->use_tc && cfg->precision == 1 && h->dh == FM_HEAD_DIM) {
+    if ((rc = dalloc_t(h, &h->qkv_bf16, BL * 3 * D)) ||
+        (rc = fmha_make_map(&h->qkv_map, h->qkv_bf16, (int)BL, D))) {
+      ps_dit_destroy(h);
+      return rc;
+    }
+    h->use_fmha = true;
+  }
   cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(attn_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   gemv_set_attr<float>();
@@ -347,9 +316,14 @@ int ps_dit_forward(ps_dit* h, const float* x, const int32_t* host_ts, int B, flo
     Epi e{};
     e.mode = EPI_STORE;
     e.bias = bw.b_qkv;
-    e.out = h->qkv;
+    e.out = h->use_fmha ? nullptr : h->qkv;
+    e.out_bf16 = h->use_fmha ? h->qkv_bf16 : nullptr;
     if ((rc = gemm(h, 4 * i + 0, h->a, aop, bw.qkv, M, 3 * D, D, e, st))) return rc;
-    if (h->use_tc && h->cfg.precision == 1 && launch_attn_tc(AM_BF16, at, B, st)) {
+    if (h->use_fmha) {
+      // bf16 path, head_dim 64: tcgen05/TMEM flash attention (attn_fmha.cuh)
+      const FmhaArgs fa{L, D, B, 1.4426950408889634f / sqrtf((float)h->dh), h->tca.o.bf16};
+      if ((rc = fmha_launch(h->qkv_map, fa, h->H, st))) return rc;
+    } else if (h->use_tc && h->cfg.precision == 1 && launch_attn_tc(AM_BF16, at, B, st)) {
       // bf16 path: tensor-core flash attention (bf16 MMA)
     } else if (h->use_tc && h->cfg.precision == 0 && launch_attn_tc(AM_TF32X3, at, B, st)) {
       // fp32 path: tensor-core flash attention (3xTF32 MMA)

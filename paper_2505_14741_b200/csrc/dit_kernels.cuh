@@ -149,6 +149,51 @@ static __global__ void patch_embed_kernel(const float* __restrict__ x, int64_t n
   }
 }
 
+// host wrappers (one launch; B rows of `in` selected by `rows`)
+template <typename TW, int MAXB>
+static inline void gemv_launch(const GemvArgs& p, cudaStream_t st) {
+  constexpr int C = GvLoad<TW>::C;
+  const size_t smem = gemv_smem<TW>(p.B, p.K);
+  launch_pdl(gemv_kernel<TW, MAXB>, dim3((p.N + 32 * C - 1) / (32 * C)), dim3(GV_WARPS * 32), smem,
+             st, p);
+}
+
+template <typename TW>
+static inline void gemv_set_attr() {
+  cudaFuncSetAttribute(gemv_kernel<TW, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
+  cudaFuncSetAttribute(gemv_kernel<TW, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
+  cudaFuncSetAttribute(gemv_kernel<TW, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
+  cudaFuncSetAttribute(gemv_kernel<TW, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
+}
+
+// W is fp32 or bf16 (wbf16), (K, N) row-major, N % (4|8) == 0
+static inline int gemv(const float* in, int64_t in_stride, const int32_t* rows, const void* W, bool wbf16,
+                const float* bias, float* out, int K, int N, int B, int act, cudaStream_t st) {
+  GemvArgs p{};
+  p.in = in;
+  p.in_stride = in_stride;
+  for (int b = 0; b < B; ++b) p.in_row[b] = rows ? rows[b] : b;
+  p.W = W;
+  p.bias = bias;
+  p.out = out;
+  p.K = K;
+  p.N = N;
+  p.B = B;
+  p.act = act;
+  if (wbf16) {
+    if (B <= 1) gemv_launch<__nv_bfloat16, 1>(p, st);
+    else if (B <= 4) gemv_launch<__nv_bfloat16, 4>(p, st);
+    else if (B <= 8) gemv_launch<__nv_bfloat16, 8>(p, st);
+    else gemv_launch<__nv_bfloat16, 16>(p, st);
+  } else {
+    if (B <= 1) gemv_launch<float, 1>(p, st);
+    else if (B <= 4) gemv_launch<float, 4>(p, st);
+    else if (B <= 8) gemv_launch<float, 8>(p, st);
+    else gemv_launch<float, 16>(p, st);
+  }
+  return check_launch("gemv");
+}
+
 // ---------------------------------------------------------------- LN + modulate
 // a[row, :] = LN(h[row, :]) * (1 + scale_b) + shift_b ; one warp per row.
 // Output formats: fp32 (out_f32), bf16 (out_bf16), or the tf32 hi/lo split

@@ -8,7 +8,7 @@
 
 namespace ps {
 
-enum EpiMode { EPI_STORE = 0, EPI_GELU = 1, EPI_RESID = 2, EPI_UNPATCH = 3 };
+enum EpiMode { EPI_STORE = 0, EPI_GELU = 1, EPI_RESID = 2, EPI_UNPATCH = 3, EPI_ADD = 4, EPI_NCHW = 5 };
 
 struct Epi {
   int mode;
@@ -27,7 +27,20 @@ struct Epi {
   DitGeom g;
   float* eps;
   int64_t n_latent;
+  // EPI_ADD (U-Net): y = act(acc + bias + vec[b(m) * vec_stride + n] + resid[m, n]),
+  // each term optional; y -> out (fp32) and/or out_bf16. b(m) = m / L.
+  const float* vec;
+  int64_t vec_stride;
+  int act;  // 1 = GELU-tanh
+  // EPI_NCHW: eps[b * n_latent + n * hw + p] = acc + bias, m = b * hw + p
+  int hw;
 };
+
+__device__ __forceinline__ float epi_add_val(const Epi& e, int m, int n, int64_t idx, float v) {
+  if (e.vec) v += e.vec[(int64_t)(m / e.L) * e.vec_stride + n];
+  if (e.resid) v += e.resid[idx];
+  return e.act ? gelu_tanh_f(v) : v;
+}
 
 __device__ __forceinline__ void epi_store(const Epi& e, int m, int n, int N, float acc) {
   const float v = acc + (e.bias ? e.bias[n] : 0.f);
@@ -58,13 +71,24 @@ __device__ __forceinline__ void epi_store(const Epi& e, int m, int n, int N, flo
       e.eps[(int64_t)b * e.n_latent + patch_elem_index(e.g, l, n)] = v;
       break;
     }
+    case EPI_ADD: {
+      const float y = epi_add_val(e, m, n, idx, v);
+      if (e.out) e.out[idx] = y;
+      if (e.out_bf16) e.out_bf16[idx] = __float2bfloat16_rn(y);
+      break;
+    }
+    case EPI_NCHW: {
+      const int b = m / e.hw, px = m % e.hw;
+      e.eps[(int64_t)b * e.n_latent + (int64_t)n * e.hw + px] = v;
+      break;
+    }
   }
 }
 
 // 16 consecutive columns n..n+15 of one row (tensor-core epilogue): 16-byte
 // vector loads/stores when the row segment is full and aligned.
 __device__ __forceinline__ void epi_store16(const Epi& e, int m, int n, int N, const float* v) {
-  const bool vec = (n + 16 <= N) && ((N & 3) == 0) && e.mode != EPI_UNPATCH;
+  const bool vec = (n + 16 <= N) && ((N & 7) == 0) && e.mode != EPI_UNPATCH && e.mode != EPI_NCHW;
   if (!vec) {
 #pragma unroll
     for (int j = 0; j < 16; ++j)
@@ -126,6 +150,40 @@ __device__ __forceinline__ void epi_store16(const Epi& e, int m, int n, int N, c
             make_float4(x[4 * q] - hi.x, x[4 * q + 1] - hi.y, x[4 * q + 2] - hi.z,
                         x[4 * q + 3] - hi.w);
       }
+    }
+  } else if (e.mode == EPI_ADD) {
+    if (e.vec) {
+      const float* vv = e.vec + (int64_t)(m / e.L) * e.vec_stride + n;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 a = *reinterpret_cast<const float4*>(vv + 4 * q);
+        x[4 * q] += a.x; x[4 * q + 1] += a.y; x[4 * q + 2] += a.z; x[4 * q + 3] += a.w;
+      }
+    }
+    if (e.resid) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 a = *reinterpret_cast<const float4*>(e.resid + base + 4 * q);
+        x[4 * q] += a.x; x[4 * q + 1] += a.y; x[4 * q + 2] += a.z; x[4 * q + 3] += a.w;
+      }
+    }
+    if (e.act)
+#pragma unroll
+      for (int j = 0; j < 16; ++j) x[j] = gelu_tanh_f(x[j]);
+    if (e.out)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<float4*>(e.out + base + 4 * q) =
+            make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+    if (e.out_bf16) {
+      uint32_t u[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(x[2 * q], x[2 * q + 1]);
+        u[q] = *reinterpret_cast<uint32_t*>(&h2);
+      }
+      *reinterpret_cast<uint4*>(e.out_bf16 + base) = make_uint4(u[0], u[1], u[2], u[3]);
+      *reinterpret_cast<uint4*>(e.out_bf16 + base + 8) = make_uint4(u[4], u[5], u[6], u[7]);
     }
   } else {  // EPI_RESID
     const float* g = e.gate + (int64_t)(m / e.L) * e.gate_stride + n;

@@ -159,9 +159,9 @@ static int choose_bn(int precision, int M, int N, int splits) {
   return 64;
 }
 
-int tc_prepare(TcWeights& w, TcActs& acts, const std::vector<const float*>& Ws,
-               const std::vector<int>& Ks, const std::vector<int>& Ns, int max_rows, int ref_rows,
-               int D, int Dm, int precision) {
+int tc_prepare_weights(TcWeights& w, const std::vector<const float*>& Ws,
+                       const std::vector<int>& Ks, const std::vector<int>& Ns,
+                       const std::vector<int>& ref_rows, int precision) {
   w.precision = precision;
   w.layers.resize(Ws.size());
   const int bk = precision == 1 ? TcCfg<KIND_BF16, 64>::BK : TcCfg<KIND_TF32X3, 64>::BK;
@@ -169,7 +169,8 @@ int tc_prepare(TcWeights& w, TcActs& acts, const std::vector<const float*>& Ws,
     TcLayer& L = w.layers[i];
     L.K = Ks[i];
     L.N = Ns[i];
-    L.splits = choose_splits(ref_rows, L.N, L.K, bk);
+    if (!Ws[i]) continue;  // placeholder (layer not run on the tensor cores)
+    L.splits = choose_splits(ref_rows[i], L.N, L.K, bk);
     const size_t n = (size_t)L.K * L.N;
     PS_CHECK_ARG(L.K % 8 == 0, "tensor-core GEMM needs K % 8 == 0");
     cudaError_t e;
@@ -196,6 +197,14 @@ int tc_prepare(TcWeights& w, TcActs& acts, const std::vector<const float*>& Ws,
       }
     }
   }
+  return 0;
+}
+
+int tc_prepare(TcWeights& w, TcActs& acts, const std::vector<const float*>& Ws,
+               const std::vector<int>& Ks, const std::vector<int>& Ns, int max_rows, int ref_rows,
+               int D, int Dm, int precision) {
+  const std::vector<int> refs(Ws.size(), ref_rows);
+  if (int rc = tc_prepare_weights(w, Ws, Ks, Ns, refs, precision)) return rc;
   if (int rc = alloc_operand(acts, acts.a, max_rows, D, precision)) return rc;
   if (int rc = alloc_operand(acts, acts.o, max_rows, D, precision)) return rc;
   if (int rc = alloc_operand(acts, acts.hid, max_rows, Dm, precision)) return rc;

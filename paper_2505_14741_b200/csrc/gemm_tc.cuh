@@ -392,6 +392,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 int tc_prepare(TcWeights& w, TcActs& acts, const std::vector<const float*>& Ws,
                const std::vector<int>& Ks, const std::vector<int>& Ns, int max_rows, int ref_rows,
                int D, int Dm, int precision);
+// weights only; ref_rows[i] = one lane's rows of layer i (fixes its split-K)
+int tc_prepare_weights(TcWeights& w, const std::vector<const float*>& Ws,
+                       const std::vector<int>& Ks, const std::vector<int>& Ns,
+                       const std::vector<int>& ref_rows, int precision);
 int tc_gemm(const TcWeights& w, int layer, const TcOperand& A, int M, int N, int K, const Epi& e,
             int precision, cudaStream_t st);
 void tc_release(TcWeights& w, TcActs& acts);

@@ -47,6 +47,10 @@ CONFIGS = {
     # warm-up 13 is the paper's CogVideoX setting (R/PAPER.md:253)
     "cogvideox_bf16": dict(spec="cogvideox_2b", precision="bf16", T=50, sigma="zero", warmup=13,
                            baseline_config=3, max_batch=4),
+    # configs[4]: AudioLDM2-large-shaped U-Net, mel latent 8x256x16, 200 steps;
+    # warm-up 1 is the paper's AudioLDM2 setting (R/PAPER.md:253)
+    "audioldm2_unet_bf16": dict(spec="audioldm2_large", family="unet", precision="bf16", T=200,
+                                sigma="zero", warmup=1, baseline_config=4),
     # the reference's own MLP at data_dim 4096 (C1-ref), fp64
     "c1ref_mlp": dict(spec=None, precision="fp64", T=50, sigma="zero", warmup=5,
                       baseline_config=0),
@@ -131,6 +135,10 @@ def build_predictor(cfg, max_batch):
         from paper_2505_14741_b200.predictor import TrainConfig, init_weights
 
         return init_weights(TrainConfig(data_dim=4096, hidden=(64, 64), embed_dim=16, seed=7))
+    if cfg.get("family") == "unet":
+        from paper_2505_14741_b200.unet import UNetWeights
+
+        return UNetWeights(cfg["spec"], seed=0, max_batch=max_batch)
     from paper_2505_14741_b200.dit import DiTWeights
 
     return DiTWeights(cfg["spec"], seed=0, precision=cfg["precision"], max_batch=max_batch)
@@ -170,6 +178,11 @@ def cpu_predictor(cfg):
 
     if cfg["spec"] is None:
         return core.MLP.init(4096, hidden=(64, 64), embed_dim=16, seed=7)
+    if cfg.get("family") == "unet":
+        from oracle.unet import UNet
+        from paper_2505_14741_b200.unet_spec import UNET_SPECS
+
+        return UNet(UNET_SPECS[cfg["spec"]], seed=0)
     from paper_2505_14741_b200.spec import SPECS
 
     return DiT(SPECS[cfg["spec"]], seed=0)
@@ -267,7 +280,14 @@ def config_block(args, cfg, world):
          "degree": world, "warmup_steps": cfg["warmup"] if world > 1 else 0,
          "precision": cfg["precision"], "l2": "flushed (512 MiB write) between timed runs",
          "parallelism": f"parastep-d{world}" if world > 1 else "sequential (degree 1)"}
-    if cfg["spec"]:
+    if cfg.get("family") == "unet":
+        from paper_2505_14741_b200.unet_spec import UNET_SPECS
+
+        s = UNET_SPECS[cfg["spec"]]
+        b.update({"predictor": cfg["spec"], "latent": f"{s.in_channels}x{s.height}x{s.width}",
+                  "channels": list(s.channels), "attention_levels": list(s.attn),
+                  "resblocks_per_level": s.layers, "transformer_depth": s.depth})
+    elif cfg["spec"]:
         s = SPECS[cfg["spec"]]
         b.update({"predictor": cfg["spec"], "latent": f"{s.channels}x{s.height}x{s.width}"
                   if s.frames == 1 else f"{s.frames}x{s.height}x{s.width}x{s.channels}",
@@ -322,7 +342,7 @@ def time_runs(sampler, K, W, flush, torch, dist, world, seed0=0):
 
 def gemm_roofline(w, cfg, torch, bf16_peak):
     """Dominant kernel: the tcgen05 GEMM of the MLP fc1 layer (M = tokens)."""
-    if cfg["spec"] is None:
+    if cfg["spec"] is None or cfg.get("family") == "unet":
         return None
     which = 2
     M, N, K = w.gemm_shape(which, 1)

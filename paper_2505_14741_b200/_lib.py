@@ -45,6 +45,19 @@ class ps_dit_weights(C.Structure):
                 ("freq_rows", C.c_int32)]
 
 
+class ps_unet_op(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in (
+        "kind", "layer", "pre", "in1", "in2", "c1", "c2", "h", "w", "taps", "resample", "cout",
+        "temb_layer", "temb_off", "resid", "out", "out_bf16", "act", "heads")] + [("eps", C.c_float)]
+
+
+class ps_unet_config(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in (
+        "in_channels", "height", "width", "groups", "freq_dim", "temb_dim", "temb_cols",
+        "max_batch", "n_ops", "n_bufs")] + [("ops", C.POINTER(ps_unet_op)),
+                                            ("bufs", C.POINTER(C.c_void_p))]
+
+
 _SIGS = {
     "ps_last_error": (C.c_char_p, []),
     "ps_version": (C.c_int, []),
@@ -75,6 +88,12 @@ _SIGS = {
     "ps_dit_kernels_per_forward": (C.c_int, [C.c_void_p]),
     "ps_dit_bench_gemm": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]),
     "ps_gemm_probe": (C.c_float, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
+    "ps_unet_create": (C.c_int, [C.POINTER(ps_unet_config), C.POINTER(ps_dit_weights),
+                                 C.POINTER(C.c_void_p)]),
+    "ps_unet_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int32), C.c_int,
+                                  C.c_void_p, C.c_void_p]),
+    "ps_unet_destroy": (C.c_int, [C.c_void_p]),
+    "ps_unet_kernels_per_forward": (C.c_int, [C.c_void_p]),
     "ps_attn_test": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
                                C.c_int, C.c_void_p]),
     "ps_attn_probe": (C.c_float, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),

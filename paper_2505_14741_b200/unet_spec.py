@@ -107,7 +107,8 @@ class Op:
     taps: int = 1            # 9 = 3x3 conv, 1 = 1x1 / linear
     resample: int = RS_NONE
     cout: int = 0
-    temb_off: int = -1       # column offset of this ResBlock's time projection
+    temb_layer: int = -1     # this ResBlock's time projection layer
+    temb_off: int = -1       # its column offset in the concatenated time table
     resid: int = -1          # buffer added in the epilogue
     out: int = -1            # output buffer id (BUF_EPS for conv_out)
     out_bf16: int = 0        # output written as bf16 (a later op's A operand)
@@ -174,7 +175,7 @@ def plan(s: UNetSpec) -> Plan:
         l1 = p.layer(f"{name}.conv1", 9 * ctot, cout)
         lt = p.layer(f"{name}.temb", T, cout)
         p.ops.append(Op(OP_CONV, l1, PRE_GN_SILU, x, x2, cin, cin2, h, w, 9, RS_NONE, cout,
-                        temb_off=toff, out=t, name=f"{name}.conv1"))
+                        temb_layer=lt, temb_off=toff, out=t, name=f"{name}.conv1"))
         l2 = p.layer(f"{name}.conv2", 9 * cout, cout)
         o = p.buf(hw * cout)
         if ctot != cout:
@@ -183,10 +184,10 @@ def plan(s: UNetSpec) -> Plan:
                             out=o, name=f"{name}.skip"))
             resid = o
         else:
+            assert x2 == -1, "a concatenated input always changes the width"
             resid = x
         p.ops.append(Op(OP_CONV, l2, PRE_GN_SILU, t, -1, cout, 0, h, w, 9, RS_NONE, cout,
                         resid=resid, out=o, name=f"{name}.conv2"))
-        del lt
         return o
 
     def transformer(name, hbuf, c, h, w):

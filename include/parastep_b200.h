@@ -161,6 +161,10 @@ int ps_gemm_test(const float* A, const float* W, const float* bias, float* C, in
 /* Diagnostic: mean device time (us) of `iters` back-to-back tensor-core
  * GEMM launches on zero operands; dbg bit0 = skip MMA, bit1 = skip TMA. */
 float ps_gemm_probe(int M, int N, int K, int precision, int dbg, int iters);
+/* Diagnostic: clock64 phase stamps of CTA (0,0,0) of the last probe launch
+ * run with dbg bit 4 (entry, prologue, PDL wait, first TMA, first stage,
+ * last stage, accumulator ready, epilogue done, exit). */
+int ps_gemm_stamps(long long* out9);
 
 /* ---- U-Net-shaped predictor (paper_2505_14741_b200/unet_spec.py) -------
  * A native executor for the op list unet_spec.plan() emits (bf16 tcgen05

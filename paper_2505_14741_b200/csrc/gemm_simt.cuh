@@ -200,6 +200,68 @@ __device__ __forceinline__ void epi_store16(const Epi& e, int m, int n, int N, c
   }
 }
 
+// 4 consecutive columns n..n+3 of one row (the split-K reduction's grain)
+__device__ __forceinline__ void epi_store4(const Epi& e, int m, int n, int N, const float* v) {
+  const bool vec = (n + 4 <= N) && ((N & 3) == 0) && e.mode != EPI_UNPATCH && e.mode != EPI_NCHW;
+  if (!vec) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (n + j < N) epi_store(e, m, n + j, N, v[j]);
+    return;
+  }
+  const int64_t base = (int64_t)m * N + n;
+  const float4 bb = e.bias ? *reinterpret_cast<const float4*>(e.bias + n)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+  float x[4] = {v[0] + bb.x, v[1] + bb.y, v[2] + bb.z, v[3] + bb.w};
+  auto st_f32 = [&](float* out) {
+    *reinterpret_cast<float4*>(out + base) = make_float4(x[0], x[1], x[2], x[3]);
+  };
+  auto st_bf16 = [&](__nv_bfloat16* out) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(x[0], x[1]), c = __floats2bfloat162_rn(x[2], x[3]);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&a);
+    u.y = *reinterpret_cast<uint32_t*>(&c);
+    *reinterpret_cast<uint2*>(out + base) = u;
+  };
+  if (e.mode == EPI_STORE) {
+    if (e.out) st_f32(e.out);
+    if (e.out_bf16) st_bf16(e.out_bf16);
+  } else if (e.mode == EPI_GELU) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) x[j] = gelu_tanh_f(x[j]);
+    if (e.out) st_f32(e.out);
+    if (e.out_bf16) st_bf16(e.out_bf16);
+    if (e.out_hi) {
+      const float4 hi = make_float4(tf32_hi(x[0]), tf32_hi(x[1]), tf32_hi(x[2]), tf32_hi(x[3]));
+      *reinterpret_cast<float4*>(e.out_hi + base) = hi;
+      *reinterpret_cast<float4*>(e.out_lo + base) =
+          make_float4(x[0] - hi.x, x[1] - hi.y, x[2] - hi.z, x[3] - hi.w);
+    }
+  } else if (e.mode == EPI_ADD) {
+    if (e.vec) {
+      const float4 a = *reinterpret_cast<const float4*>(e.vec + (int64_t)(m / e.L) * e.vec_stride + n);
+      x[0] += a.x; x[1] += a.y; x[2] += a.z; x[3] += a.w;
+    }
+    if (e.resid) {
+      const float4 a = *reinterpret_cast<const float4*>(e.resid + base);
+      x[0] += a.x; x[1] += a.y; x[2] += a.z; x[3] += a.w;
+    }
+    if (e.act)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) x[j] = gelu_tanh_f(x[j]);
+    if (e.out) st_f32(e.out);
+    if (e.out_bf16) st_bf16(e.out_bf16);
+  } else {  // EPI_RESID
+    const float4 g = *reinterpret_cast<const float4*>(e.gate + (int64_t)(m / e.L) * e.gate_stride + n);
+    float4 r = *reinterpret_cast<const float4*>(e.resid + base);
+    r.x = fmaf(g.x, x[0], r.x);
+    r.y = fmaf(g.y, x[1], r.y);
+    r.z = fmaf(g.z, x[2], r.z);
+    r.w = fmaf(g.w, x[3], r.w);
+    *reinterpret_cast<float4*>(e.resid + base) = r;
+  }
+}
+
 constexpr int SG_BM = 64, SG_BN = 64, SG_BK = 16;
 
 static __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict__ A,

@@ -302,7 +302,7 @@ int ps_gemm_test(const float* A, const float* W, const float* bias, float* Cout,
 float ps_gemm_probe(int M, int N, int K, int precision, int dbg, int iters) {
   g_split_enable = (dbg & 32) ? 0 : 1;  // bit 5: disable split-K
   g_force_in_cta = (dbg & 64) ? 1 : 0;  // bit 6: segments in-CTA
-  dbg &= 15;
+  dbg &= 31;
   float *A = nullptr, *W = nullptr, *C = nullptr;
   if (cudaMalloc(&A, (size_t)M * K * 4) || cudaMalloc(&W, (size_t)K * N * 4) ||
       cudaMalloc(&C, (size_t)M * N * 4))
@@ -342,6 +342,18 @@ float ps_gemm_probe(int M, int N, int K, int precision, int dbg, int iters) {
   g_split_enable = 1;
   g_force_in_cta = 0;
   return us;
+}
+
+// Diagnostic: clock64 phase stamps of CTA (0,0,0) from the last probe run
+// with dbg bit 4 set: [entry, prologue done, PDL wait done, first TMA
+// issued, first stage landed (MMA), last stage landed, accumulator ready,
+// epilogue done, exit].
+int ps_gemm_stamps(long long* out9) {
+  long long h[16];
+  cudaError_t e = cudaMemcpyFromSymbol(h, g_tc_ts, sizeof(h));
+  if (e != cudaSuccess) return fail((int)e, "stamps");
+  for (int i = 0; i < 9; ++i) out9[i] = h[i];
+  return 0;
 }
 
 }  // extern "C"

@@ -208,6 +208,14 @@ __device__ __forceinline__ void cluster_sync_all() {
                    : "memory");
 }
 
+// diagnostics: dbg bit 4 records clock64() phase stamps of CTA (0,0,0) here
+__device__ long long g_tc_ts[16];
+#define TC_STAMP(i)                                                     \
+  do {                                                                  \
+    if ((dbg & 16) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) \
+      g_tc_ts[i] = clock64();                                           \
+  } while (0)
+
 template <int KIND, int BN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapAlo,
@@ -235,6 +243,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint32_t tcols = 32;
   while (tcols < (uint32_t)((in_cta ? S : 1) * BN)) tcols <<= 1;
   if (dbg & 8) return;  // probe: launch floor only
+  if (threadIdx.x == 0) TC_STAMP(0);
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&mapA);
@@ -260,9 +269,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) TC_STAMP(1);
   // the prologue above overlaps the predecessor's tail (PDL); operands and
   // epilogue inputs are only touched after it completes
   pdl_wait_and_release();
+  if (threadIdx.x == 0) TC_STAMP(2);
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer
@@ -275,6 +286,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         continue;
       }
       mbar_expect_tx(&full[s], C::STAGE_BYTES);
+      if (kb == 0) TC_STAMP(3);
       const int kx = (kb0 + kb) * C::BK;
       tma_load_2d(st, &mapA, &full[s], kx, m0);
       tma_load_2d(st + C::A_BYTES, &mapB, &full[s], kx, n0);
@@ -297,6 +309,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int s = kb % TC_STAGES;
       mbar_wait(&full[s], (kb / TC_STAGES) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (kb == 0) TC_STAMP(4);
+      if (kb == nk - 1) TC_STAMP(5);
       uint8_t* st = smem + s * C::STAGE_BYTES;
       const uint64_t a0 = smem_desc_sw128(st);
       const uint64_t b0 = smem_desc_sw128(st + C::A_BYTES);
@@ -329,6 +343,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // ---------------- epilogue: TMEM -> registers -> fused store
   mbar_wait(accum, 0);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (threadIdx.x == 0) TC_STAMP(6);
   const int row = m0 + warp * 32 + lane;
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
   if (in_cta) {
@@ -359,33 +374,34 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     }
     cluster_sync_all();
+    // CTA z reduces rows [z*128/S, (z+1)*128/S) over DSMEM in segment order,
+    // one float4 per thread per pass (all S remote loads issued before the sum)
     const int rows = TC_BM / S, r0 = blockIdx.z * rows;
-    const int chunks = rows * (BN / 16);
+    const int chunks = rows * (BN / 4);
     for (int idx = threadIdx.x; idx < chunks; idx += TC_THREADS) {
-      const int r = r0 + idx / (BN / 16), c = (idx % (BN / 16)) * 16;
-      float v[16];
+      const int r = r0 + idx / (BN / 4), c = (idx % (BN / 4)) * 4;
+      float4 a[8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float4 a = ld_dsmem_f4(part + r * PST + c + 4 * q, 0);
-        v[4 * q] = a.x; v[4 * q + 1] = a.y; v[4 * q + 2] = a.z; v[4 * q + 3] = a.w;
-      }
-      for (int s = 1; s < S; ++s) {
+      for (int s = 0; s < 8; ++s)
+        if (s < S) a[s] = ld_dsmem_f4(part + r * PST + c, (uint32_t)s);
+      float v[4] = {a[0].x, a[0].y, a[0].z, a[0].w};
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float4 a = ld_dsmem_f4(part + r * PST + c + 4 * q, (uint32_t)s);
-          v[4 * q] += a.x; v[4 * q + 1] += a.y; v[4 * q + 2] += a.z; v[4 * q + 3] += a.w;
+      for (int s = 1; s < 8; ++s)
+        if (s < S) {
+          v[0] += a[s].x; v[1] += a[s].y; v[2] += a[s].z; v[3] += a[s].w;
         }
-      }
-      if (m0 + r < M && n0 + c < N) epi_store16(e, m0 + r, n0 + c, N, v);
+      if (m0 + r < M && n0 + c < N) epi_store4(e, m0 + r, n0 + c, N, v);
     }
     cluster_sync_all();  // peers' smem stays live until every CTA has read it
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  if (threadIdx.x == 0) TC_STAMP(7);
   __syncthreads();
   if (warp == 2) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(tcols));
   }
+  if (threadIdx.x == 0) TC_STAMP(8);
 }
 
 // ------------------------------------------------------------------ host side

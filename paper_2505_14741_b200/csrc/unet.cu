@@ -11,6 +11,7 @@
 // time projection and the residual. Transformers reuse the DiT pieces
 // (LN producer, tcgen05 attention, GELU epilogue).
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -26,6 +27,7 @@ enum { UOP_CONV = 0, UOP_LINEAR = 1, UOP_ATTN = 2 };
 enum { PRE_NONE = 0, PRE_CONVERT = 1, PRE_GN = 2, PRE_GN_SILU = 3, PRE_LN = 4 };
 enum { RS_NONE = 0, RS_DOWN = 1, RS_UP = 2 };
 constexpr int BUF_LATENT = -2, BUF_EPS = -3;
+constexpr int GN_MAX_SLICES = 32;
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
@@ -34,13 +36,18 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
 
 // ---------------------------------------------------------------- GroupNorm statistics
 // stats[(b*G + g)*2 + {0,1}] = mean, rstd over the group's channels of the
-// (virtual) concatenation [in1 | in2] and all pixels; two passes over the
-// L2-resident input, fixed-order block reduction (deterministic).
+// (virtual) concatenation [in1 | in2] and all pixels. Grid (G, B, S): block
+// s takes a contiguous slice of the group's elements and writes its exact
+// two-pass partial (count, mean, M2); the last block of the group to finish
+// (atomic ticket) merges the S partials in slice order with Chan's formula.
+// The result never depends on which block is last: deterministic.
 struct GnArgs {
   const float* in1;
   const float* in2;
-  int c1, c2, hw, G;
+  int c1, c2, hw, G, S;
   float eps;
+  float* partial;     // [B*G][S][3]
+  unsigned* ticket;   // [B*G], zero between launches
   float* stats;
 };
 
@@ -57,12 +64,14 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return t;
 }
 
-static __global__ void __launch_bounds__(512) gn_stats_kernel(const __grid_constant__ GnArgs p) {
+static __global__ void __launch_bounds__(256) gn_stats_kernel(const __grid_constant__ GnArgs p) {
   __shared__ float red[32];
+  __shared__ bool last;
   pdl_wait_and_release();
-  const int g = blockIdx.x, b = blockIdx.y;
+  const int g = blockIdx.x, b = blockIdx.y, sl = blockIdx.z;
   const int ctot = p.c1 + p.c2, cpg = ctot / p.G;
   const int64_t n = (int64_t)p.hw * cpg;
+  const int64_t i0 = n * sl / p.S, i1 = n * (sl + 1) / p.S;
   auto val = [&](int64_t idx) -> float {
     const int64_t px = idx / cpg;
     const int c = g * cpg + (int)(idx % cpg);
@@ -70,17 +79,39 @@ static __global__ void __launch_bounds__(512) gn_stats_kernel(const __grid_const
     return c < p.c1 ? p.in1[row * p.c1 + c] : p.in2[row * p.c2 + (c - p.c1)];
   };
   float s = 0.f;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += val(i);
-  const float mean = block_sum(s, red) / (float)n;
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) s += val(i);
+  const float cnt = (float)(i1 - i0);
+  const float mean = block_sum(s, red) / cnt;
   float q = 0.f;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
     const float d = val(i) - mean;
     q = fmaf(d, d, q);
   }
-  const float var = block_sum(q, red) / (float)n;
+  const float m2 = block_sum(q, red);
+  const int bg = b * p.G + g;
   if (threadIdx.x == 0) {
-    p.stats[(b * p.G + g) * 2] = mean;
-    p.stats[(b * p.G + g) * 2 + 1] = rsqrtf(var + p.eps);
+    float* pp = p.partial + ((int64_t)bg * p.S + sl) * 3;
+    pp[0] = cnt;
+    pp[1] = mean;
+    pp[2] = m2;
+    __threadfence();
+    last = atomicAdd(&p.ticket[bg], 1u) == (unsigned)(p.S - 1);
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    const volatile float* pp = p.partial + (int64_t)bg * p.S * 3;
+    double na = pp[0], ma = pp[1], qa = pp[2];
+    for (int k = 1; k < p.S; ++k) {  // Chan et al. pairwise merge, slice order
+      const double nb = pp[3 * k], mb = pp[3 * k + 1], qb = pp[3 * k + 2];
+      const double nn = na + nb, d = mb - ma;
+      ma += d * nb / nn;
+      qa += qb + d * d * na * nb / nn;
+      na = nn;
+    }
+    p.stats[bg * 2] = (float)ma;
+    p.stats[bg * 2 + 1] = rsqrtf((float)(qa / na) + p.eps);
+    p.ticket[bg] = 0u;  // re-arm for the next launch / graph replay
   }
 }
 
@@ -186,6 +217,8 @@ struct ps_unet {
   std::vector<void*> owned;
   __nv_bfloat16* scratch = nullptr;  // im2col / producer output
   float* stats = nullptr;            // GroupNorm statistics
+  float* gn_partial = nullptr;       // [B*G][GN_MAX_SLICES][3]
+  unsigned* gn_ticket = nullptr;     // [B*G]
   float* zero_mod = nullptr;         // LN without modulation
   float *t1 = nullptr, *emb = nullptr, *temb = nullptr, *temb_b = nullptr;
   __nv_bfloat16* temb_w = nullptr;   // (temb_dim, temb_cols) bf16, all ResBlock projections
@@ -260,6 +293,9 @@ int ps_unet_create(const ps_unet_config* cfg, const ps_dit_weights* w, ps_unet**
   if ((rc = tc_prepare_weights(h->tcw, Ws, Ks, Ns, refs, 1))) return bail(rc);
   if ((rc = ualloc(h, (void**)&h->scratch, scratch * 2 + 256)) ||
       (rc = ualloc(h, (void**)&h->stats, (size_t)MB * cfg->groups * 2 * sizeof(float))) ||
+      (rc = ualloc(h, (void**)&h->gn_partial,
+                   (size_t)MB * cfg->groups * GN_MAX_SLICES * 3 * sizeof(float))) ||
+      (rc = ualloc(h, (void**)&h->gn_ticket, (size_t)MB * cfg->groups * sizeof(unsigned))) ||
       (rc = ualloc(h, (void**)&h->zero_mod, 4096 * sizeof(float))) ||
       (rc = ualloc(h, (void**)&h->t1, (size_t)MB * cfg->temb_dim * sizeof(float))) ||
       (rc = ualloc(h, (void**)&h->emb, (size_t)MB * cfg->temb_dim * sizeof(float))) ||
@@ -267,6 +303,7 @@ int ps_unet_create(const ps_unet_config* cfg, const ps_dit_weights* w, ps_unet**
       (rc = ualloc(h, (void**)&h->temb_b, (size_t)cfg->temb_cols * sizeof(float) + 256)))
     return bail(rc);
   cudaMemset(h->zero_mod, 0, 4096 * sizeof(float));
+  cudaMemset(h->gn_ticket, 0, (size_t)MB * cfg->groups * sizeof(unsigned));
   // concatenate every ResBlock's time projection into one (temb_dim, temb_cols) matrix
   {
     float* tw = nullptr;
@@ -350,8 +387,14 @@ int ps_unet_forward(ps_unet* h, const float* x, const int32_t* host_ts, int B, f
     const float* in1 = op.in1 == BUF_LATENT ? x : buf(op.in1);
     // ---- A operand
     if (op.pre == PRE_GN || op.pre == PRE_GN_SILU) {
-      GnArgs g{in1, buf(op.in2), op.c1, op.c2, op.h * op.w, c.groups, op.eps, h->stats};
-      launch_pdl(gn_stats_kernel, dim3(c.groups, B), dim3(512), 0, st, g);
+      // slices: ~2 blocks per SM for one lane, >= 1024 elements each; never a
+      // function of B, so a lane's statistics are the same bits in any batch
+      const int64_t n = (int64_t)op.h * op.w * ((op.c1 + op.c2) / c.groups);
+      int S = (int)std::min<int64_t>(GN_MAX_SLICES, std::max<int64_t>(1, n / 1024));
+      S = std::max(1, std::min(S, (2 * 148 + c.groups - 1) / c.groups));
+      GnArgs g{in1, buf(op.in2), op.c1, op.c2, op.h * op.w, c.groups, S, op.eps,
+               h->gn_partial, h->gn_ticket, h->stats};
+      launch_pdl(gn_stats_kernel, dim3(c.groups, B, S), dim3(256), 0, st, g);
       if ((rc = check_launch("gn_stats"))) return rc;
       ++launches;
     }

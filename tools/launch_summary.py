@@ -4,7 +4,7 @@ import csv
 import sys
 
 
-def summarise(path, top=25):
+def summarise(path, top=25, by_grid=False):
     rows = list(csv.reader(open(path)))
     hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hdr]
@@ -15,7 +15,9 @@ def summarise(path, top=25):
             continue
         v = float(r[vi].replace(",", ""))
         v *= {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}[r[ui]]
-        name = r[ki].split("(")[0][:70]
+        name = r[ki].split("(")[0][:52]
+        if by_grid:
+            name = f"{name} {r[h.index('Grid Size')]}"[:70]
         tot[name] += v
         cnt[name] += 1
     T = sum(tot.values())
@@ -28,4 +30,5 @@ def summarise(path, top=25):
 
 
 if __name__ == "__main__":
-    print(summarise(sys.argv[1]))
+    print(summarise(sys.argv[1], top=40 if "--by-grid" in sys.argv else 25,
+                    by_grid="--by-grid" in sys.argv))

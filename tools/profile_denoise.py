@@ -19,8 +19,12 @@ ap.add_argument("--config", default="small_dit_fp32")
 ap.add_argument("--degree", type=int, default=1)
 ap.add_argument("--strategy", default=None)
 ap.add_argument("--runs", type=int, default=1)
+ap.add_argument("--steps", type=int, default=None, help="override T (fewer forwards under ncu)")
 a = ap.parse_args()
-cfg = bench.CONFIGS[a.config]
+cfg = dict(bench.CONFIGS[a.config])
+if a.steps:
+    cfg["T"] = a.steps
+    cfg["warmup"] = min(cfg["warmup"], a.steps - 1)
 w = bench.build_predictor(cfg, max_batch=8)
 sched = make_default_schedule(cfg["T"], cfg["sigma"])
 rc = bench.run_cfg(cfg, w.data_dim, a.degree, a.strategy)

@@ -1,6 +1,7 @@
 // Host side of the tcgen05 flash attention (attn_fmha.cuh) plus C-ABI
 // diagnostics that run one attention against caller buffers.
 
+#include <algorithm>
 #include <cmath>
 #include <mutex>
 
@@ -9,17 +10,25 @@
 
 namespace ps {
 
-int fmha_make_map(CUtensorMap* m, const __nv_bfloat16* qkv_bf16, int rows, int D) {
-  return tc_make_map(m, qkv_bf16, 2, 3 * D, rows, FM_BK);
+int fmha_make_map(CUtensorMap* m, const __nv_bfloat16* qkv_bf16, int rows, int cols) {
+  return tc_make_map(m, qkv_bf16, 2, cols, rows, FM_BK);
 }
 
-int fmha_launch(const CUtensorMap& map, const FmhaArgs& a, int H, cudaStream_t st) {
+template <int DH>
+static cudaError_t fmha_go(const CUtensorMap& map, const FmhaArgs& a, cudaStream_t st) {
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(fmha_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FM_SMEM);
+    cudaFuncSetAttribute(fmha_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         FmCfg<DH>::SMEM);
   });
-  cudaError_t e = launch_pdl(fmha_tc_kernel, dim3((a.L + FM_BQ - 1) / FM_BQ, H, a.B),
-                             dim3(FM_THREADS), FM_SMEM, st, map, a);
+  return launch_pdl(fmha_tc_kernel<DH>, dim3((a.L + FM_BQ - 1) / FM_BQ, a.H, a.B),
+                    dim3(FM_THREADS), FmCfg<DH>::SMEM, st, map, a);
+}
+
+int fmha_launch(const CUtensorMap& map, const FmhaArgs& a, cudaStream_t st) {
+  const int DH = fmha_padded_dim(a.dh);
+  if (DH == 0) return fail(PS_EUNSUP, "tcgen05 attention: head_dim must be a multiple of 8, <= 128");
+  cudaError_t e = DH == 64 ? fmha_go<64>(map, a, st) : fmha_go<128>(map, a, st);
   if (e != cudaSuccess) return fail((int)e, std::string("fmha: ") + cudaGetErrorString(e));
   return check_launch("fmha");
 }
@@ -27,6 +36,18 @@ int fmha_launch(const CUtensorMap& map, const FmhaArgs& a, int H, cudaStream_t s
 static __global__ void f32_to_bf16_n(const float* in, __nv_bfloat16* out, int64_t n) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = __float2bfloat16_rn(in[i]);
+}
+
+// fp32 [rows, 3, H, dh] -> bf16 [rows, 3, H, DH], zero-padded head dims
+static __global__ void pad_qkv_bf16(const float* in, __nv_bfloat16* out, int64_t rows, int H,
+                                    int dh, int DH) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t per = (int64_t)3 * H * DH;
+  if (i >= rows * per) return;
+  const int64_t r = i / per;
+  const int j = (int)(i % per), wh = j / DH, d = j % DH;
+  out[i] = d < dh ? __float2bfloat16_rn(in[r * 3 * H * dh + (int64_t)wh * dh + d])
+                  : __float2bfloat16_rn(0.f);
 }
 
 static __global__ void bf16_to_f32_n(const __nv_bfloat16* in, float* out, int64_t n) {
@@ -40,13 +61,15 @@ static __global__ void bf16_to_f32_n(const __nv_bfloat16* in, float* out, int64_
 // launches instead (qkv/out may then be null). Allocates; test/probe only.
 static float attn_run(const float* qkv, float* out, int B, int L, int H, int D, int impl,
                       int iters, cudaStream_t st, int* rc_out) {
-  const int dh = D / H;
+  const int dh = D / H, DH = fmha_padded_dim(dh);
   const int64_t nq = (int64_t)B * L * 3 * D, no = (int64_t)B * L * D;
+  const int64_t nqp = (int64_t)B * L * 3 * H * (DH ? DH : 1);
   __nv_bfloat16 *qb = nullptr, *ob = nullptr;
   float* qf = nullptr;
   int rc = 0;
   float us = -1.f;
-  if (cudaMalloc(&qb, nq * 2) || cudaMalloc(&ob, no * 2) || cudaMalloc(&qf, nq * 4)) {
+  if (cudaMalloc(&qb, std::max(nq, nqp) * 2) || cudaMalloc(&ob, no * 2) ||
+      cudaMalloc(&qf, nq * 4)) {
     rc = fail(PS_ECUDA, "attn_run: cudaMalloc");
   }
   if (!rc) {
@@ -54,16 +77,19 @@ static float attn_run(const float* qkv, float* out, int B, int L, int H, int D, 
       f32_to_bf16_n<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(qkv, qb, nq);
       // the mma.sync kernel reads fp32 qkv: give it the bf16-rounded values
       bf16_to_f32_n<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(qb, qf, nq);
+      if (impl == 2 && DH)
+        pad_qkv_bf16<<<(unsigned)((nqp + 255) / 256), 256, 0, st>>>(qf, qb, (int64_t)B * L, H, dh,
+                                                                     DH);
     } else {
-      cudaMemsetAsync(qb, 0, nq * 2, st);
+      cudaMemsetAsync(qb, 0, std::max(nq, nqp) * 2, st);
       cudaMemsetAsync(qf, 0, nq * 4, st);
     }
     CUtensorMap map;
     if (impl == 2) {
-      if (dh != FM_DH) rc = fail(PS_EUNSUP, "tcgen05 attention needs head_dim 64");
-      else rc = fmha_make_map(&map, qb, B * L, D);
+      if (!DH) rc = fail(PS_EUNSUP, "tcgen05 attention: unsupported head_dim");
+      else rc = fmha_make_map(&map, qb, B * L, 3 * H * DH);
     }
-    FmhaArgs fa{L, D, B, 1.4426950408889634f / sqrtf((float)dh), ob};
+    FmhaArgs fa{L, D, B, H, dh, 1.4426950408889634f / sqrtf((float)dh), ob};
     AttnArgs aa{};
     aa.qkv = qf;
     aa.L = L;
@@ -73,7 +99,7 @@ static float attn_run(const float* qkv, float* out, int B, int L, int H, int D, 
     aa.scale = 1.0f / sqrtf((float)dh);
     aa.out_bf16 = ob;
     auto go = [&]() -> int {
-      if (impl == 2) return fmha_launch(map, fa, H, st);
+      if (impl == 2) return fmha_launch(map, fa, st);
       if (!launch_attn_tc(AM_BF16, aa, B, st)) return fail(PS_EUNSUP, "head_dim unsupported");
       return check_launch("attn_tc");
     };

@@ -27,15 +27,23 @@
 
 namespace ps {
 
-constexpr int FM_BQ = 128, FM_BK = 128, FM_DH = FM_HEAD_DIM, FM_STAGES = 3;
+constexpr int FM_BQ = 128, FM_BK = 128;
 constexpr int FM_THREADS = 192;
-constexpr int FM_TILE = 128 * 128;                 // bytes of one 128 x 64 bf16 tile
-constexpr int FM_Q_OFF = 0;
-constexpr int FM_KV_OFF = FM_TILE;                 // stage s: K at +2s*TILE, V at +(2s+1)*TILE
-constexpr int FM_P_OFF = FM_KV_OFF + 2 * FM_STAGES * FM_TILE;  // 2 buffers x 2 atom columns
-constexpr int FM_BAR_OFF = FM_P_OFF + 4 * FM_TILE;
-constexpr int FM_SMEM = FM_BAR_OFF + 256 + 1024;
-constexpr uint32_t FM_TMEM_COLS = 512;             // S0 [0,128) S1 [128,256) O [256,320)
+constexpr int FM_TILE = 128 * 128;  // bytes of one 128-row x 128-byte (64 bf16) box
+
+// DH = padded head width in smem/TMEM (64, or 128 for head_dim 72..128):
+// NA = DH/64 swizzle atoms along the head dim per Q/K/V tile.
+template <int DH>
+struct FmCfg {
+  static constexpr int NA = DH / 64;
+  static constexpr int STAGES = DH == 64 ? 3 : 2;
+  static constexpr int Q_OFF = 0;
+  static constexpr int KV_OFF = NA * FM_TILE;  // stage s: K at +2s*NA*TILE, V at +(2s+1)*NA*TILE
+  static constexpr int P_OFF = KV_OFF + 2 * STAGES * NA * FM_TILE;  // 2 buffers x 2 key atoms
+  static constexpr int BAR_OFF = P_OFF + 4 * FM_TILE;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  static constexpr uint32_t TMEM_COLS = 512;  // S0 [0,128) S1 [128,256) O [256, 256+DH)
+};
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   uint32_t r[32];
@@ -78,8 +86,13 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
+template <int DH>
 __global__ void __launch_bounds__(FM_THREADS, 1)
     fmha_tc_kernel(const __grid_constant__ CUtensorMap mapQKV, const __grid_constant__ FmhaArgs p) {
+  using C = FmCfg<DH>;
+  constexpr int NA = C::NA, FM_STAGES = C::STAGES, FM_Q_OFF = C::Q_OFF, FM_KV_OFF = C::KV_OFF,
+                FM_P_OFF = C::P_OFF, FM_BAR_OFF = C::BAR_OFF;
+  constexpr uint32_t FM_TMEM_COLS = C::TMEM_COLS;
   extern __shared__ __align__(1024) uint8_t fm_smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(fm_smem_raw) + 1023) & ~uintptr_t(1023));
@@ -129,32 +142,40 @@ __global__ void __launch_bounds__(FM_THREADS, 1)
   if (warp == 4) {
     if (lane == 0) {
       // ---------------- TMA producer
-      mbar_expect_tx(q_full, FM_TILE);
-      tma_load_2d(smem + FM_Q_OFF, &mapQKV, q_full, head * FM_DH, row_base + q0);
+      // column of (which, head, atom a) in the [rows, 3*H*DH] operand
+      const int hc = head * DH, wstride = p.H * DH;
+      mbar_expect_tx(q_full, NA * FM_TILE);
+      for (int a = 0; a < NA; ++a)
+        tma_load_2d(smem + FM_Q_OFF + a * FM_TILE, &mapQKV, q_full, hc + 64 * a, row_base + q0);
       for (int j = 0; j < nkb; ++j) {
         const int s = j % FM_STAGES;
         mbar_wait(&kv_empty[s], ((j / FM_STAGES) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[s], 2 * FM_TILE);
-        uint8_t* st = smem + FM_KV_OFF + 2 * s * FM_TILE;
-        tma_load_2d(st, &mapQKV, &kv_full[s], p.D + head * FM_DH, row_base + j * FM_BK);
-        tma_load_2d(st + FM_TILE, &mapQKV, &kv_full[s], 2 * p.D + head * FM_DH,
-                    row_base + j * FM_BK);
+        mbar_expect_tx(&kv_full[s], 2 * NA * FM_TILE);
+        uint8_t* st = smem + FM_KV_OFF + 2 * s * NA * FM_TILE;
+        for (int a = 0; a < NA; ++a) {
+          tma_load_2d(st + a * FM_TILE, &mapQKV, &kv_full[s], wstride + hc + 64 * a,
+                      row_base + j * FM_BK);
+          tma_load_2d(st + (NA + a) * FM_TILE, &mapQKV, &kv_full[s], 2 * wstride + hc + 64 * a,
+                      row_base + j * FM_BK);
+        }
       }
     }
   } else if (warp == 5) {
     if (lane == 0) {
       // ---------------- MMA issuer
       constexpr uint32_t idS = make_idesc(KIND_BF16, 128, 128);
-      constexpr uint32_t idPV = make_idesc(KIND_BF16, 128, FM_DH) | (1u << 16);  // B (V) MN-major
-      const uint64_t qd = smem_desc_sw128(smem + FM_Q_OFF);
+      constexpr uint32_t idPV = make_idesc(KIND_BF16, 128, DH) | (1u << 16);  // B (V) MN-major
       auto issue_s = [&](int j) {
         const int s = j % FM_STAGES;
         mbar_wait(&kv_full[s], (j / FM_STAGES) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint64_t kd = smem_desc_sw128(smem + FM_KV_OFF + 2 * s * FM_TILE);
+        const uint8_t* kt = smem + FM_KV_OFF + 2 * s * NA * FM_TILE;
 #pragma unroll
-        for (int k = 0; k < FM_DH / 16; ++k)  // +32 B along K inside the swizzle atom
-          umma<KIND_BF16>(tS[j & 1], qd + 2 * k, kd + 2 * k, idS, k > 0 ? 1u : 0u);
+        for (int k = 0; k < DH / 16; ++k) {  // atom k/4, +32 B along K inside it
+          const uint64_t qd = smem_desc_sw128(smem + FM_Q_OFF + (k >> 2) * FM_TILE) + 2 * (k & 3);
+          const uint64_t kd = smem_desc_sw128(kt + (k >> 2) * FM_TILE) + 2 * (k & 3);
+          umma<KIND_BF16>(tS[j & 1], qd, kd, idS, k > 0 ? 1u : 0u);
+        }
         umma_commit(&s_full[j & 1]);
       };
       mbar_wait(q_full, 0);
@@ -165,7 +186,10 @@ __global__ void __launch_bounds__(FM_THREADS, 1)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const int s = j % FM_STAGES;
         const uint8_t* pb = smem + FM_P_OFF + (j & 1) * 2 * FM_TILE;
-        const uint64_t vd = smem_desc_sw128(smem + FM_KV_OFF + (2 * s + 1) * FM_TILE);
+        // V: MN-major, NA atoms of 64 dims at FM_TILE stride (LBO), 8-key groups at 1 KB (SBO)
+        const uint64_t vd = (smem_desc_sw128(smem + FM_KV_OFF + (2 * s + 1) * NA * FM_TILE) &
+                             ~(0x3FFFull << 16)) |
+                            ((uint64_t)(FM_TILE >> 4) << 16);
 #pragma unroll
         for (int k = 0; k < FM_BK / 16; ++k) {
           // P: K-major, keys [64a, 64a+64) in atom column a; V: MN-major, 16 keys = 2048 B
@@ -213,7 +237,7 @@ __global__ void __launch_bounds__(FM_THREADS, 1)
           l *= f;
           m_ref = m_tgt;
 #pragma unroll
-          for (int c = 0; c < FM_DH / 32; ++c) {
+          for (int c = 0; c < DH / 32; ++c) {
             float o[32];
             tmem_ld32(tO + lane_off + c * 32, o);
             tmem_ld_wait();
@@ -252,15 +276,16 @@ __global__ void __launch_bounds__(FM_THREADS, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const float inv = 1.f / l;
     const bool ok = q0 + r < L;
-    __nv_bfloat16* orow = p.out_bf16 + (int64_t)(row_base + q0 + r) * p.D + head * FM_DH;
+    __nv_bfloat16* orow = p.out_bf16 + (int64_t)(row_base + q0 + r) * p.D + head * p.dh;
 #pragma unroll
-    for (int c = 0; c < FM_DH / 32; ++c) {
+    for (int c = 0; c < DH / 32; ++c) {
       float o[32];
       tmem_ld32(tO + lane_off + c * 32, o);
       tmem_ld_wait();
       if (ok) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
+          if (c * 32 + 8 * q >= p.dh) break;  // padded dims (dh % 8 == 0)
           uint4 u;
           u.x = pack_bf16(o[8 * q] * inv, o[8 * q + 1] * inv);
           u.y = pack_bf16(o[8 * q + 2] * inv, o[8 * q + 3] * inv);

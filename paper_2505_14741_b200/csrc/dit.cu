@@ -44,6 +44,7 @@ struct ps_dit {
   bool use_tc;
   // bf16 path, head_dim 64: QKV GEMM writes bf16 Q/K/V, tcgen05 attention
   bool use_fmha = false;
+  int fm_dh = 0;  // padded head width of the tcgen05 attention operand
   __nv_bfloat16* qkv_bf16 = nullptr;
   CUtensorMap qkv_map;
   double flops;
@@ -209,12 +210,16 @@ int ps_dit_create(const ps_dit_config* cfg, const ps_dit_weights* w, ps_dit** ou
       return rc;
     }
   }
-  if (h->use_tc && cfg->precision == 1 && h->dh == FM_HEAD_DIM) {
-    if ((rc = dalloc_t(h, &h->qkv_bf16, BL * 3 * D)) ||
-        (rc = fmha_make_map(&h->qkv_map, h->qkv_bf16, (int)BL, D))) {
+  h->fm_dh = fmha_padded_dim(h->dh);
+  if (h->use_tc && cfg->precision == 1 && h->fm_dh) {
+    // Q/K/V in [rows, 3, H, DH] bf16 with the head dim zero-padded to DH
+    const size_t cols = (size_t)3 * h->H * h->fm_dh;
+    if ((rc = dalloc_t(h, &h->qkv_bf16, BL * cols)) ||
+        (rc = fmha_make_map(&h->qkv_map, h->qkv_bf16, (int)BL, (int)cols))) {
       ps_dit_destroy(h);
       return rc;
     }
+    cudaMemset(h->qkv_bf16, 0, BL * cols * sizeof(__nv_bfloat16));
     h->use_fmha = true;
   }
   cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -318,11 +323,16 @@ int ps_dit_forward(ps_dit* h, const float* x, const int32_t* host_ts, int B, flo
     e.bias = bw.b_qkv;
     e.out = h->use_fmha ? nullptr : h->qkv;
     e.out_bf16 = h->use_fmha ? h->qkv_bf16 : nullptr;
+    if (h->use_fmha && h->fm_dh != h->dh) {
+      e.pad_dh = h->dh;
+      e.pad_DH = h->fm_dh;
+    }
     if ((rc = gemm(h, 4 * i + 0, h->a, aop, bw.qkv, M, 3 * D, D, e, st))) return rc;
     if (h->use_fmha) {
       // bf16 path, head_dim 64: tcgen05/TMEM flash attention (attn_fmha.cuh)
-      const FmhaArgs fa{L, D, B, 1.4426950408889634f / sqrtf((float)h->dh), h->tca.o.bf16};
-      if ((rc = fmha_launch(h->qkv_map, fa, h->H, st))) return rc;
+      const FmhaArgs fa{L, D, B, h->H, h->dh, 1.4426950408889634f / sqrtf((float)h->dh),
+                        h->tca.o.bf16};
+      if ((rc = fmha_launch(h->qkv_map, fa, st))) return rc;
     } else if (h->use_tc && h->cfg.precision == 1 && launch_attn_tc(AM_BF16, at, B, st)) {
       // bf16 path: tensor-core flash attention (bf16 MMA)
     } else if (h->use_tc && h->cfg.precision == 0 && launch_attn_tc(AM_TF32X3, at, B, st)) {

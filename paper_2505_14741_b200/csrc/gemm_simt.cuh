@@ -34,7 +34,14 @@ struct Epi {
   int act;  // 1 = GELU-tanh
   // EPI_NCHW: eps[b * n_latent + n * hw + p] = acc + bias, m = b * hw + p
   int hw;
+  // EPI_STORE bf16 into a head-padded operand: column n = (w*H + h)*pad_dh + d
+  // goes to (w*H + h)*pad_DH + d of a row of N/pad_dh*pad_DH (0 = dense)
+  int pad_dh, pad_DH;
 };
+
+__device__ __forceinline__ int64_t padded_index(const Epi& e, int m, int n, int N) {
+  return (int64_t)m * (N / e.pad_dh * e.pad_DH) + (n / e.pad_dh) * e.pad_DH + n % e.pad_dh;
+}
 
 __device__ __forceinline__ float epi_add_val(const Epi& e, int m, int n, int64_t idx, float v) {
   if (e.vec) v += e.vec[(int64_t)(m / e.L) * e.vec_stride + n];
@@ -48,7 +55,7 @@ __device__ __forceinline__ void epi_store(const Epi& e, int m, int n, int N, flo
   switch (e.mode) {
     case EPI_STORE:
       if (e.out) e.out[idx] = v;
-      if (e.out_bf16) e.out_bf16[idx] = __float2bfloat16_rn(v);
+      if (e.out_bf16) e.out_bf16[e.pad_DH ? padded_index(e, m, n, N) : idx] = __float2bfloat16_rn(v);
       break;
     case EPI_GELU: {
       const float g = gelu_tanh_f(v);
@@ -88,7 +95,8 @@ __device__ __forceinline__ void epi_store(const Epi& e, int m, int n, int N, flo
 // 16 consecutive columns n..n+15 of one row (tensor-core epilogue): 16-byte
 // vector loads/stores when the row segment is full and aligned.
 __device__ __forceinline__ void epi_store16(const Epi& e, int m, int n, int N, const float* v) {
-  const bool vec = (n + 16 <= N) && ((N & 7) == 0) && e.mode != EPI_UNPATCH && e.mode != EPI_NCHW;
+  const bool vec = (n + 16 <= N) && ((N & 7) == 0) && e.mode != EPI_UNPATCH &&
+                   e.mode != EPI_NCHW && (!e.pad_DH || e.mode == EPI_STORE);
   if (!vec) {
 #pragma unroll
     for (int j = 0; j < 16; ++j)
@@ -119,8 +127,11 @@ __device__ __forceinline__ void epi_store16(const Epi& e, int m, int n, int N, c
         __nv_bfloat162 h2 = __floats2bfloat162_rn(x[2 * q], x[2 * q + 1]);
         u[q] = *reinterpret_cast<uint32_t*>(&h2);
       }
-      *reinterpret_cast<uint4*>(e.out_bf16 + base) = make_uint4(u[0], u[1], u[2], u[3]);
-      *reinterpret_cast<uint4*>(e.out_bf16 + base + 8) = make_uint4(u[4], u[5], u[6], u[7]);
+      // head-padded operand: each 8-column group lies inside one head (dh % 8 == 0)
+      const int64_t i0 = e.pad_DH ? padded_index(e, m, n, N) : base;
+      const int64_t i1 = e.pad_DH ? padded_index(e, m, n + 8, N) : base + 8;
+      *reinterpret_cast<uint4*>(e.out_bf16 + i0) = make_uint4(u[0], u[1], u[2], u[3]);
+      *reinterpret_cast<uint4*>(e.out_bf16 + i1) = make_uint4(u[4], u[5], u[6], u[7]);
     }
   } else if (e.mode == EPI_GELU) {
 #pragma unroll
@@ -202,7 +213,8 @@ __device__ __forceinline__ void epi_store16(const Epi& e, int m, int n, int N, c
 
 // 4 consecutive columns n..n+3 of one row (the split-K reduction's grain)
 __device__ __forceinline__ void epi_store4(const Epi& e, int m, int n, int N, const float* v) {
-  const bool vec = (n + 4 <= N) && ((N & 3) == 0) && e.mode != EPI_UNPATCH && e.mode != EPI_NCHW;
+  const bool vec = (n + 4 <= N) && ((N & 3) == 0) && e.mode != EPI_UNPATCH &&
+                   e.mode != EPI_NCHW && (!e.pad_DH || e.mode == EPI_STORE);
   if (!vec) {
 #pragma unroll
     for (int j = 0; j < 4; ++j)
@@ -221,7 +233,7 @@ __device__ __forceinline__ void epi_store4(const Epi& e, int m, int n, int N, co
     uint2 u;
     u.x = *reinterpret_cast<uint32_t*>(&a);
     u.y = *reinterpret_cast<uint32_t*>(&c);
-    *reinterpret_cast<uint2*>(out + base) = u;
+    *reinterpret_cast<uint2*>(out + (e.pad_DH ? padded_index(e, m, n, N) : base)) = u;
   };
   if (e.mode == EPI_STORE) {
     if (e.out) st_f32(e.out);

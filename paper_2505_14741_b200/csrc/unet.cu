@@ -286,7 +286,7 @@ int ps_unet_create(const ps_unet_config* cfg, const ps_dit_weights* w, ps_unet**
       refs[op.layer] = s.Ho * s.Wo;
       if (op.pre != PRE_NONE) scratch = std::max(scratch, (size_t)MB * s.Ho * s.Wo * s.K);
     } else {
-      PS_CHECK_ARG(op.heads * FM_HEAD_DIM == op.c1, "attention needs head_dim 64");
+      PS_CHECK_ARG(op.heads * 64 == op.c1, "attention needs head_dim 64");
     }
     h->steps.push_back(s);
   }
@@ -332,7 +332,7 @@ int ps_unet_create(const ps_unet_config* cfg, const ps_dit_weights* w, ps_unet**
     if (op.kind == UOP_ATTN) {
       PS_CHECK_ARG(op.in1 >= 0 && op.in1 < cfg->n_bufs && op.out >= 0, "attention buffers");
       if ((rc = fmha_make_map(&s.attn_map, (const __nv_bfloat16*)h->bufs[op.in1],
-                              MB * op.h * op.w, op.c1)))
+                              MB * op.h * op.w, 3 * op.c1)))
         return bail(rc);
       continue;
     }
@@ -378,9 +378,9 @@ int ps_unet_forward(ps_unet* h, const float* x, const int32_t* host_ts, int B, f
     const ps_unet_op& op = s.op;
     const int rows = B * s.Ho * s.Wo;
     if (op.kind == UOP_ATTN) {
-      const FmhaArgs fa{op.h * op.w, op.c1, B, 1.4426950408889634f / sqrtf((float)FM_HEAD_DIM),
+      const FmhaArgs fa{op.h * op.w, op.c1, B, op.heads, 64, 1.4426950408889634f / 8.0f,
                         (__nv_bfloat16*)h->bufs[op.out]};
-      if ((rc = fmha_launch(s.attn_map, fa, op.heads, st))) return rc;
+      if ((rc = fmha_launch(s.attn_map, fa, st))) return rc;
       ++launches;
       continue;
     }

@@ -54,6 +54,17 @@ def test_attention_vs_torch(B, L, H, impl):
     _check(_attn(qkv, B, L, H, D, impl), _ref(qkv, B, L, H, D))
 
 
+# head dims the tcgen05 kernel zero-pads to a 64/128-wide operand: DiT-XL/2's
+# 72, the tiny specs' 32, and the widest 128
+@pytest.mark.parametrize("dh", [32, 48, 72, 96, 128])
+@pytest.mark.parametrize("B,L,H", [(1, 256, 3), (2, 300, 2)])
+def test_attention_padded_head_dims(dh, B, L, H):
+    D = dh * H
+    g = torch.Generator(device="cuda").manual_seed(B * 1000 + L * 7 + H)
+    qkv = torch.randn((B * L, 3 * D), device="cuda", generator=g)
+    _check(_attn(qkv, B, L, H, D, 2), _ref(qkv, B, L, H, D))
+
+
 def test_attention_peaked_scores_rescale():
     """Large, drifting logits force the lazy O rescale (max jumps > 2^8)."""
     B, L, H = 1, 1536, 2

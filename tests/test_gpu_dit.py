@@ -81,7 +81,7 @@ def test_dit_forward_fp32_vs_oracle(name, bias, impl):
     _dit_eps_close(name, bias, "fp32", impl, 1e-5)
 
 
-@pytest.mark.parametrize("name", ["dit_tiny", "dit_s2", "dit_long_video"])
+@pytest.mark.parametrize("name", ["dit_tiny", "dit_s2", "dit_long_video", "dit_xl2"])
 def test_dit_forward_bf16_vs_oracle(name):
     errs = _dit_eps_close(name, 0.0, "bf16", "tcgen05", 5e-2)
     print(f"bf16 {name} eps rel-MAE vs fp64 oracle: {errs}")

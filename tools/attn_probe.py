@@ -11,6 +11,7 @@ from paper_2505_14741_b200 import _lib  # noqa: E402
 
 lib = _lib.load(require_gpu=True)
 SHAPES = [("cogvideox_2b", 1, 17550, 30, 1920), ("dit_s2 bf16 L=256", 1, 256, 6, 384),
+          ("dit_xl2 L=256 dh=72", 1, 256, 16, 1152), ("dit_xl2 x8 lanes", 8, 256, 16, 1152),
           ("L=4096 H=16", 1, 4096, 16, 1024), ("L=8192 H=8", 2, 8192, 8, 512)]
 print(f"{'shape':24s} {'impl':>4s} {'us':>10s} {'TFLOP/s':>8s}")
 for name, B, L, H, D in SHAPES:

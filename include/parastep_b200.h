@@ -165,6 +165,9 @@ float ps_gemm_probe(int M, int N, int K, int precision, int dbg, int iters);
  * run with dbg bit 4 (entry, prologue, PDL wait, first TMA, first stage,
  * last stage, accumulator ready, epilogue done, exit). */
 int ps_gemm_stamps(long long* out9);
+/* Tuning knob: minimum K-blocks per split-K segment for layers prepared
+ * afterwards (default 4); returns the previous value. */
+int ps_gemm_tune(int split_min_kb);
 
 /* ---- U-Net-shaped predictor (paper_2505_14741_b200/unet_spec.py) -------
  * A native executor for the op list unet_spec.plan() emits (bf16 tcgen05

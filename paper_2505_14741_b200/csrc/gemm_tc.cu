@@ -63,6 +63,19 @@ __global__ void transpose_convert_kernel(const float* __restrict__ W, int K, int
   }
 }
 
+int tc_operand_maps(TcOperand& op, int precision) {
+  for (int i = 0; i < 3; ++i) {
+    const int box = TC_BM >> i;  // multicast slice of 128 / CN rows
+    if (precision == 1) {
+      if (int rc = tc_make_map(&op.map_main[i], op.bf16, 2, op.cols, op.rows, box)) return rc;
+    } else {
+      if (int rc = tc_make_map(&op.map_main[i], op.hi, 4, op.cols, op.rows, box)) return rc;
+      if (int rc = tc_make_map(&op.map_lo[i], op.lo, 4, op.cols, op.rows, box)) return rc;
+    }
+  }
+  return 0;
+}
+
 static int alloc_operand(TcActs& acts, TcOperand& op, int rows, int cols, int precision) {
   op.rows = rows;
   op.cols = cols;
@@ -73,7 +86,7 @@ static int alloc_operand(TcActs& acts, TcOperand& op, int rows, int cols, int pr
     if (e != cudaSuccess) return fail((int)e, "cudaMalloc operand");
     acts.owned.push_back(op.bf16);
     cudaMemset(op.bf16, 0, n * 2);
-    return tc_make_map(&op.map_main, op.bf16, 2, cols, rows, TC_BM);
+    return tc_operand_maps(op, precision);
   }
   e = cudaMalloc(&op.hi, n * 4);
   if (e == cudaSuccess) {
@@ -84,13 +97,18 @@ static int alloc_operand(TcActs& acts, TcOperand& op, int rows, int cols, int pr
   acts.owned.push_back(op.lo);
   cudaMemset(op.hi, 0, n * 4);
   cudaMemset(op.lo, 0, n * 4);
-  if (int rc = tc_make_map(&op.map_main, op.hi, 4, cols, rows, TC_BM)) return rc;
-  return tc_make_map(&op.map_lo, op.lo, 4, cols, rows, TC_BM);
+  return tc_operand_maps(op, precision);
 }
+
+static int cluster_cap(int s) { return s <= 2 ? 148 : 128; }  // co-resident CTAs
 
 static int g_dbg = 0;  // ps_gemm_probe only
 static int g_split_enable = 1;  // probe bit 5 disables split-K
 static int g_force_in_cta = 0;  // probe bit 6 runs the segments in-CTA (no cluster)
+static int g_sc_max = 8;        // test hook: cap on cluster CTAs along K (forces the hybrid)
+// A multicast across N-tile CTAs: measured slower than independent loads at
+// every DiT/U-Net shape on B200 (profiles/), so off unless a probe asks for it
+static int g_cn_max = 1;        // probe: bit 9 = up to 4 CTAs share A, bit 8 = up to 2
 
 static int bn_index(int bn) { return bn == 32 ? 0 : (bn == 64 ? 1 : 2); }
 
@@ -107,11 +125,28 @@ static int launch(const TcLayer& L, const TcOperand& A, int M, int N, int K, con
   // segments as a cluster only while the whole grid is co-resident (clusters
   // of 4/8 leave some SMs unusable, hence the lower cap); else in-CTA
   const int tiles = tiles_n * tiles_m;
-  const bool as_cluster =
-      L.splits > 1 && tiles * L.splits <= (L.splits == 2 ? 148 : 128) && !g_force_in_cta;
-  const TcSplit sk{L.splits, as_cluster ? L.splits : 1};
+  // K segments over as many cluster CTAs SC (| S) as stay co-resident, each
+  // CTA running S/SC segments whose partial tiles fit its drained ring
+  int sc = 1;
+  if (!g_force_in_cta) {
+    const size_t ring = (size_t)C::STAGES * C::STAGE_BYTES;
+    const size_t ptile = (size_t)TC_BM * (BN + 4) * sizeof(float);
+    for (int c = L.splits < g_sc_max ? L.splits : g_sc_max; c > 1; c /= 2) {
+      if (tiles * c <= cluster_cap(c) && (size_t)(L.splits / c) * ptile <= ring) {
+        sc = c;
+        break;
+      }
+    }
+  }
+  // A multicast: CN adjacent N-tile CTAs share each A tile (one 128/CN-row
+  // slice loaded per CTA, broadcast to the group); cluster (CN, 1, sc) <= 8
+  int cn = 1;
+  while (cn * 2 <= g_cn_max && cn * 2 * sc <= 8 && tiles_n >= cn * 2) cn *= 2;
+  if ((L.splits / sc) * BN > 512)
+    return fail(PS_EUNSUP, "gemm_tc: segment accumulators exceed the 512 TMEM columns");
+  const TcSplit sk{L.splits, sc, cn};
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(tiles_n, tiles_m, sk.cluster);
+  cfg.gridDim = dim3((tiles_n + cn - 1) / cn * cn, tiles_m, sk.cluster);
   cfg.blockDim = dim3(TC_THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
@@ -119,43 +154,93 @@ static int launch(const TcLayer& L, const TcOperand& A, int M, int N, int K, con
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   at[1].id = cudaLaunchAttributeClusterDimension;
-  at[1].val.clusterDim.x = 1;
+  at[1].val.clusterDim.x = cn;
   at[1].val.clusterDim.y = 1;
   at[1].val.clusterDim.z = sk.cluster;
   cfg.attrs = at;
-  cfg.numAttrs = sk.cluster > 1 ? 2 : 1;
-  const int bi = bn_index(BN);
+  cfg.numAttrs = (sk.cluster > 1 || cn > 1) ? 2 : 1;
+  const int bi = bn_index(BN), ai = cn == 1 ? 0 : (cn == 2 ? 1 : 2);
   cudaError_t err;
   if (KIND == KIND_BF16)
-    err = cudaLaunchKernelEx(&cfg, gemm_tc_kernel<KIND, BN>, A.map_main, A.map_main, L.map_b[bi],
-                             L.map_b[bi], M, N, K, e, g_dbg, sk);
+    err = cudaLaunchKernelEx(&cfg, gemm_tc_kernel<KIND, BN>, A.map_main[ai], A.map_main[ai],
+                             L.map_b[bi], L.map_b[bi], M, N, K, e, g_dbg, sk);
   else
-    err = cudaLaunchKernelEx(&cfg, gemm_tc_kernel<KIND, BN>, A.map_main, A.map_lo, L.map_b[bi],
-                             L.map_blo[bi], M, N, K, e, g_dbg, sk);
+    err = cudaLaunchKernelEx(&cfg, gemm_tc_kernel<KIND, BN>, A.map_main[ai], A.map_lo[ai],
+                             L.map_b[bi], L.map_blo[bi], M, N, K, e, g_dbg, sk);
   if (err != cudaSuccess) return fail((int)err, std::string("gemm_tc: ") + cudaGetErrorString(err));
   return check_launch("gemm_tc");
 }
 
-// Split-K factor from the one-lane shape (ref_rows) with 64-wide tiles: grow
-// the cluster while it still fits the 148 SMs and every split keeps >= 4
-// K-blocks. Fixed per layer, so a row's accumulation order never depends on
-// the batch (forward_batch == mapped forward, bitwise).
-static int choose_splits(int ref_rows, int N, int K, int bk) {
-  const int tiles = ((ref_rows + TC_BM - 1) / TC_BM) * ((N + 63) / 64);
-  const int nk = (K + bk - 1) / bk;
+// Tile plan. At small M the mainloop is bound by per-SM TMA ingest
+// (~70 GB/s/SM measured, profiles/): a CTA loads K/S x (128 + BN) operand
+// elements, so wide N tiles (less re-reading of the shared A tile) plus
+// split-K to fill the SMs beat narrow tiles. The planner scores every
+// (BN, S) that fits co-resident (S <= 8 as one DSMEM cluster) by
+//   ingest bytes per CTA + DSMEM reduction bytes (S > 1) + cluster-sync cost
+// and keeps the cheapest. S is fixed per layer from the one-lane shape
+// (ref_rows), so a row's accumulation order never depends on the batch
+// (forward_batch == mapped forward, bitwise); BN may change per call.
+static int g_split_min_kb = 2;  // ps_gemm_tune: K-blocks each split keeps at least (tf3x)
+
+
+struct TilePlan {
+  int bn, splits;
+};
+
+// bf16 (2 B/element): ingest matters less than the DSMEM reduction, which
+// measured slower than modelled; the narrow-tile policy below wins there:
+// split while the grid (64-wide tiles) stays co-resident and each split keeps
+// >= 4 K-blocks, then 32-wide tiles when the grid covers <= half the SMs.
+static TilePlan plan_tiles_bf16(int M, int N, int K) {
+  const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + 63) / 64);
+  const int nk = (K + 63) / 64;
   int s = 1;
-  while (s < 8 && tiles * s * 2 <= (s == 1 ? 148 : 128) && nk / (s * 2) >= 4) s *= 2;
-  return g_split_enable ? s : 1;
+  while (s < 8 && tiles * s * 2 <= cluster_cap(s * 2) && nk / (s * 2) >= 4) s *= 2;
+  if (!g_split_enable) s = 1;
+  return TilePlan{2 * tiles * s <= cluster_cap(s) ? 32 : 64, s};
 }
 
-// N-tile width per call: narrow 32-wide tiles when the grid would cover at
-// most half the SMs, 128-wide (bf16) for large grids. Any width gives the
-// same per-element accumulation order.
-static int choose_bn(int precision, int M, int N, int splits) {
-  const int t64 = ((M + TC_BM - 1) / TC_BM) * ((N + 63) / 64);
-  const int cap = splits <= 2 ? 148 : 128;  // co-resident CTAs for this cluster size
-  if (2 * t64 * splits <= cap) return 32;
-  if (precision == 1 && t64 > 600 && splits <= 4) return 128;  // TMEM: S x 128 <= 512
+static TilePlan plan_tiles(int precision, int M, int N, int K) {
+  if (precision == 1) return plan_tiles_bf16(M, N, K);
+  const int bk = precision == 1 ? 64 : 32;       // K elements per 128-byte stage row
+  const double esz = precision == 1 ? 2.0 : 8.0;  // bytes per element incl. the tf32 lo copy
+  const int nk = (K + bk - 1) / bk, tm = (M + TC_BM - 1) / TC_BM;
+  TilePlan best{64, 1};
+  double best_cost = 1e300;
+  const int bns[3] = {128, 64, 32};
+  for (int bn : bns) {
+    const int tn = (N + bn - 1) / bn;
+    for (int s = 1; s <= 8; s *= 2) {
+      if (s > 1 && (tm * tn * s > cluster_cap(s) || nk / s < g_split_min_kb)) break;
+      const int ctas = tm * tn * s;
+      const int waves = (ctas + 147) / 148;
+      double cost = waves * ((double)((nk + s - 1) / s) * bk * (128 + bn) * esz);
+      if (s > 1) cost += 128.0 * bn * 4 + 40e3;  // DSMEM partial tile + 2 cluster syncs
+      if (cost < best_cost * 0.97) {  // prefer the earlier (wider / fewer-split) plan on ties
+        best_cost = cost;
+        best = TilePlan{bn, s};
+      }
+    }
+  }
+  if (!g_split_enable) best.splits = 1;
+  return best;
+}
+
+// N-tile width per call, for the layer's fixed split count: the planned
+// width when the call is the planned shape, else narrow tiles for small
+// grids and wide ones for large grids (in-CTA segments need S x BN <= 512
+// TMEM columns). Any width gives the same per-element accumulation order.
+static int choose_bn(const TcLayer& L, int precision, int M, int N) {
+  const int splits = L.splits;
+  const int tm = (M + TC_BM - 1) / TC_BM;
+  auto fits = [&](int bn) {
+    const int tiles = tm * ((N + bn - 1) / bn);
+    return splits == 1 || tiles * splits <= cluster_cap(splits) || splits * bn <= 512;
+  };
+  if (M <= L.ref_rows && fits(L.bn)) return L.bn;
+  const int t64 = tm * ((N + 63) / 64);
+  if (2 * t64 * splits <= cluster_cap(splits)) return 32;
+  if (t64 > 600 && splits * 128 <= 512) return 128;
   return 64;
 }
 
@@ -164,13 +249,15 @@ int tc_prepare_weights(TcWeights& w, const std::vector<const float*>& Ws,
                        const std::vector<int>& ref_rows, int precision) {
   w.precision = precision;
   w.layers.resize(Ws.size());
-  const int bk = precision == 1 ? TcCfg<KIND_BF16, 64>::BK : TcCfg<KIND_TF32X3, 64>::BK;
   for (size_t i = 0; i < Ws.size(); ++i) {
     TcLayer& L = w.layers[i];
     L.K = Ks[i];
     L.N = Ns[i];
     if (!Ws[i]) continue;  // placeholder (layer not run on the tensor cores)
-    L.splits = choose_splits(ref_rows[i], L.N, L.K, bk);
+    const TilePlan tp = plan_tiles(precision, ref_rows[i], L.N, L.K);
+    L.splits = tp.splits;
+    L.bn = tp.bn;
+    L.ref_rows = ref_rows[i];
     const size_t n = (size_t)L.K * L.N;
     PS_CHECK_ARG(L.K % 8 == 0, "tensor-core GEMM needs K % 8 == 0");
     cudaError_t e;
@@ -191,7 +278,7 @@ int tc_prepare_weights(TcWeights& w, const std::vector<const float*>& Ws,
     for (int bi = 0; bi < 3; ++bi) {
       if (precision == 1) {
         if (int rc = tc_make_map(&L.map_b[bi], L.w_main, 2, L.K, L.N, boxes[bi])) return rc;
-      } else if (bi < 2) {
+      } else {
         if (int rc = tc_make_map(&L.map_b[bi], L.w_main, 4, L.K, L.N, boxes[bi])) return rc;
         if (int rc = tc_make_map(&L.map_blo[bi], L.w_lo, 4, L.K, L.N, boxes[bi])) return rc;
       }
@@ -214,13 +301,14 @@ int tc_prepare(TcWeights& w, TcActs& acts, const std::vector<const float*>& Ws,
 int tc_gemm(const TcWeights& w, int layer, const TcOperand& A, int M, int N, int K, const Epi& e,
             int precision, cudaStream_t st) {
   const TcLayer& L = w.layers[layer];
-  const int bn = choose_bn(precision, M, N, L.splits);
+  const int bn = choose_bn(L, precision, M, N);
   if (precision == 1) {
     if (bn == 32) return launch<KIND_BF16, 32>(L, A, M, N, K, e, st);
     if (bn == 128) return launch<KIND_BF16, 128>(L, A, M, N, K, e, st);
     return launch<KIND_BF16, 64>(L, A, M, N, K, e, st);
   }
   if (bn == 32) return launch<KIND_TF32X3, 32>(L, A, M, N, K, e, st);
+  if (bn == 128) return launch<KIND_TF32X3, 128>(L, A, M, N, K, e, st);
   return launch<KIND_TF32X3, 64>(L, A, M, N, K, e, st);
 }
 
@@ -265,8 +353,10 @@ int ps_gemm_test(const float* A, const float* W, const float* bias, float* Cout,
   cudaStream_t st = as_stream(cs);
   // impl 3: tensor cores with the K segments forced in-CTA (cluster-free);
   // must equal impl 2 bit-for-bit (test_gemm_split_paths_bitwise)
+  // impl 4: at most 2 cluster CTAs along K (each running S/2 segments)
   g_force_in_cta = impl == 3 ? 1 : 0;
-  if (impl == 3) impl = 2;
+  g_sc_max = impl == 4 ? 2 : 8;
+  if (impl == 3 || impl == 4) impl = 2;
   Epi e{};
   e.mode = EPI_STORE;
   e.bias = bias;
@@ -292,6 +382,7 @@ int ps_gemm_test(const float* A, const float* W, const float* bias, float* Cout,
   if (!rc && se != cudaSuccess) rc = fail((int)se, std::string("gemm_test: ") + cudaGetErrorString(se));
   tc_release(w, acts);
   g_force_in_cta = 0;
+  g_sc_max = 8;
   return rc;
 }
 
@@ -302,6 +393,7 @@ int ps_gemm_test(const float* A, const float* W, const float* bias, float* Cout,
 float ps_gemm_probe(int M, int N, int K, int precision, int dbg, int iters) {
   g_split_enable = (dbg & 32) ? 0 : 1;  // bit 5: disable split-K
   g_force_in_cta = (dbg & 64) ? 1 : 0;  // bit 6: segments in-CTA
+  g_cn_max = (dbg & 512) ? 4 : ((dbg & 256) ? 2 : 1);
   dbg &= 31;
   float *A = nullptr, *W = nullptr, *C = nullptr;
   if (cudaMalloc(&A, (size_t)M * K * 4) || cudaMalloc(&W, (size_t)K * N * 4) ||
@@ -341,7 +433,16 @@ float ps_gemm_probe(int M, int N, int K, int precision, int dbg, int iters) {
   cudaFree(C);
   g_split_enable = 1;
   g_force_in_cta = 0;
+  g_cn_max = 1;
   return us;
+}
+
+// Tuning knob (diagnostic): minimum K-blocks per split-K segment; affects
+// layers prepared afterwards. Returns the previous value.
+int ps_gemm_tune(int split_min_kb) {
+  const int prev = g_split_min_kb;
+  if (split_min_kb >= 1) g_split_min_kb = split_min_kb;
+  return prev;
 }
 
 // Diagnostic: clock64 phase stamps of CTA (0,0,0) from the last probe run

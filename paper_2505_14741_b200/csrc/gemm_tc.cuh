@@ -33,8 +33,10 @@ struct TcOperand {
   float* hi = nullptr;
   float* lo = nullptr;
   int rows = 0, cols = 0;
-  CUtensorMap map_main;  // bf16 or hi
-  CUtensorMap map_lo;
+  // A maps per multicast width CN = 1, 2, 4 (boxes of 128/CN rows): index
+  // log2(CN). [0] of map_main is the full 128-row box. bf16 or hi / tf32-lo.
+  CUtensorMap map_main[3];
+  CUtensorMap map_lo[3];
 };
 
 struct TcActs {
@@ -50,6 +52,8 @@ struct TcLayer {
   // are the tf32-lo copies of the 3xTF32 path
   CUtensorMap map_b[3], map_blo[3];
   int splits = 1;  // split-K factor, fixed per layer (independent of M: batch == single bitwise)
+  int bn = 64;     // planned N-tile width at ref_rows
+  int ref_rows = 0;
 };
 
 struct TcWeights {
@@ -59,7 +63,7 @@ struct TcWeights {
 
 constexpr int TC_BM = 128;
 constexpr int TC_THREADS = 128;
-constexpr int TC_STAGES = 4;
+constexpr int TC_SMEM_BUDGET = 200 * 1024;  // stage ring per CTA
 
 // ------------------------------------------------------------------ PTX
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -93,6 +97,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+
+// multicast: the box lands at the same smem offset in every CTA of cta_mask
+// and signals each one's mbarrier at the same offset
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                               int x, int y, uint16_t cta_mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "h"(cta_mask)
       : "memory");
 }
 
@@ -144,6 +159,23 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// arrive on the same-offset mbarrier of every CTA in cta_mask once the
+// previously issued MMAs complete
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t cta_mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(cta_mask)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(cta));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+               : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   uint32_t r[16];
   asm volatile(
@@ -169,7 +201,12 @@ struct TcCfg {
   static constexpr int B_BYTES = BN * BK_BYTES;
   static constexpr int NOPS = KIND == KIND_BF16 ? 1 : 2;  // main (+lo) copies
   static constexpr int STAGE_BYTES = NOPS * (A_BYTES + B_BYTES);
-  static constexpr int SMEM = TC_STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  // as many stages as the budget holds (3..6; tf3x BN=128 takes 3 x 64 KB).
+  // Measured: deeper rings (up to 10) do not speed up the small-M mainloop,
+  // which is bound by per-SM TMA ingest (~70 GB/s/SM), not latency x depth
+  static constexpr int STAGES_FIT = TC_SMEM_BUDGET / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_FIT < 3 ? 3 : (STAGES_FIT > 6 ? 6 : STAGES_FIT);
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
 };
 
@@ -187,8 +224,10 @@ struct TcCfg {
 //                 accumulators and adds them in the same order.
 struct TcSplit {
   int splits;   // S: K segments (fixed per layer)
-  int cluster;  // 1 (segments in-CTA) or S (one CTA per segment)
+  int cluster;  // SC: CTAs along K per tile (1 = all segments in one CTA; S/SC each)
+  int cn;       // N-tile CTAs per cluster sharing one multicast A tile (1, 2, 4)
 };
+// cluster dims (cn, 1, cluster): rank = x + cn * z
 
 __device__ __forceinline__ float4 ld_dsmem_f4(const float* local, uint32_t cta) {
   uint32_t remote;
@@ -226,6 +265,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int TC_STAGES = C::STAGES;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + TC_STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + TC_STAGES;
   uint64_t* accum = empty + TC_STAGES;
@@ -233,15 +273,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * BN;
+  const int CN = sk.cn, cx = blockIdx.x % CN;
+  // A multicast group: the CN N-tile CTAs of this K segment
+  const uint16_t grp = (uint16_t)(((1u << CN) - 1u) << (CN * (sk.cluster > 1 ? blockIdx.z : 0)));
   const int nk_all = (K + C::BK - 1) / C::BK;
   const int S = sk.splits;
-  const bool in_cta = sk.cluster == 1;  // all segments in this CTA
-  const int kb0 = in_cta ? 0 : (int)((int64_t)blockIdx.z * nk_all / S);
-  const int kb1 = in_cta ? nk_all : (int)((int64_t)(blockIdx.z + 1) * nk_all / S);
+  const int SC = sk.cluster;            // CTAs sharing the K range (1 = all in this CTA)
+  const int G = S / SC;                 // consecutive segments per CTA
+  const bool in_cta = SC == 1;
+  const int zc = in_cta ? 0 : (int)blockIdx.z;
+  auto seg_lo = [&](int sg) { return (int)((int64_t)sg * nk_all / S); };
+  const int kb0 = seg_lo(zc * G), kb1 = seg_lo((zc + 1) * G);
   const int nk = kb1 - kb0;
-  // TMEM columns: one BN-wide accumulator per in-CTA segment (power of 2 >= 32)
+  // TMEM columns: one BN-wide accumulator per segment of this CTA (power of 2 >= 32)
   uint32_t tcols = 32;
-  while (tcols < (uint32_t)((in_cta ? S : 1) * BN)) tcols <<= 1;
+  while (tcols < (uint32_t)(G * BN)) tcols <<= 1;
   if (dbg & 8) return;  // probe: launch floor only
   if (threadIdx.x == 0) TC_STAMP(0);
 
@@ -254,7 +300,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int s = 0; s < TC_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CN);  // every CTA of the multicast group releases the stage
     }
     mbar_init(accum, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -269,6 +315,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  if (CN > 1) cluster_sync_all();  // peers' barriers initialised before any multicast
   if (threadIdx.x == 0) TC_STAMP(1);
   // the prologue above overlaps the predecessor's tail (PDL); operands and
   // epilogue inputs are only touched after it completes
@@ -288,22 +335,30 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_expect_tx(&full[s], C::STAGE_BYTES);
       if (kb == 0) TC_STAMP(3);
       const int kx = (kb0 + kb) * C::BK;
-      tma_load_2d(st, &mapA, &full[s], kx, m0);
-      tma_load_2d(st + C::A_BYTES, &mapB, &full[s], kx, n0);
-      if (KIND == KIND_TF32X3) {
-        tma_load_2d(st + C::A_BYTES + C::B_BYTES, &mapAlo, &full[s], kx, m0);
-        tma_load_2d(st + 2 * C::A_BYTES + C::B_BYTES, &mapBlo, &full[s], kx, n0);
+      if (CN == 1) {
+        tma_load_2d(st, &mapA, &full[s], kx, m0);
+        if (KIND == KIND_TF32X3) tma_load_2d(st + C::A_BYTES + C::B_BYTES, &mapAlo, &full[s], kx, m0);
+      } else {
+        // this CTA's 128/CN-row slice of the shared A tile, to the whole group
+        const int rs = TC_BM / CN, ro = cx * rs;
+        tma_load_2d_mc(st + ro * 128, &mapA, &full[s], kx, m0 + ro, grp);
+        if (KIND == KIND_TF32X3)
+          tma_load_2d_mc(st + C::A_BYTES + C::B_BYTES + ro * 128, &mapAlo, &full[s], kx, m0 + ro,
+                         grp);
       }
+      tma_load_2d(st + C::A_BYTES, &mapB, &full[s], kx, n0);
+      if (KIND == KIND_TF32X3)
+        tma_load_2d(st + 2 * C::A_BYTES + C::B_BYTES, &mapBlo, &full[s], kx, n0);
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer
     constexpr uint32_t idesc = make_idesc(KIND, TC_BM, BN);
-    int seg = 0, seg_end = in_cta ? (int)((int64_t)nk_all / S) : nk, seg_start = 0;
+    int seg = 0, seg_start = 0, seg_end = seg_lo(zc * G + 1) - kb0;
     for (int kb = 0; kb < nk; ++kb) {
-      if (kb == seg_end) {  // next in-CTA segment: fresh accumulator columns
+      if (kb == seg_end) {  // next segment of this CTA: fresh accumulator columns
         ++seg;
         seg_start = kb;
-        seg_end = (int)((int64_t)(seg + 1) * nk_all / S);
+        seg_end = seg_lo(zc * G + seg + 1) - kb0;
       }
       const uint32_t dacc = tmem + (uint32_t)(seg * BN);
       const int s = kb % TC_STAGES;
@@ -315,7 +370,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const uint64_t a0 = smem_desc_sw128(st);
       const uint64_t b0 = smem_desc_sw128(st + C::A_BYTES);
       if (dbg & 1) {
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+        for (int c = 0; c < CN; ++c)
+          mbar_arrive_remote(&empty[s], (uint32_t)(__ffs(grp) - 1 + c));
         continue;
       }
 #pragma unroll
@@ -331,7 +387,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           umma<KIND>(dacc, alo + koff, b0 + koff, idesc, 1u);
         }
       }
-      umma_commit(&empty[s]);
+      if (CN == 1) umma_commit(&empty[s]);
+      else umma_commit_mc(&empty[s], grp);
     }
     if (dbg & 1)
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(accum)) : "memory");
@@ -359,36 +416,48 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       if ((dbg & 4) == 0 && row < M && n0 + c < N) epi_store16(e, row, n0 + c, N, v);
     }
+    if (CN > 1) cluster_sync_all();  // peers' last multicast commits have landed on our barriers
   } else {
-    // partial tile -> own smem (stage ring is drained: all MMAs completed)
+    // this CTA's G segment partials -> own smem (the stage ring is drained:
+    // all MMAs completed, every multicast into it has landed)
     constexpr int PST = BN + 4;  // row stride (floats), keeps 16-B alignment
+    constexpr int PTILE = TC_BM * PST;
     float* part = reinterpret_cast<float*>(smem);
     const int rloc = warp * 32 + lane;
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 16) {
+    for (int c = 0; c < G * BN; c += 16) {  // segment c / BN -> partial tile c / BN
       float v[16];
       tmem_ld16(trow + c, v);
+      float* dst = part + (c / BN) * PTILE + rloc * PST + (c % BN);
 #pragma unroll
       for (int q = 0; q < 4; ++q)
-        *reinterpret_cast<float4*>(part + rloc * PST + c + 4 * q) =
+        *reinterpret_cast<float4*>(dst + 4 * q) =
             make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     }
     cluster_sync_all();
-    // CTA z reduces rows [z*128/S, (z+1)*128/S) over DSMEM in segment order,
-    // one float4 per thread per pass (all S remote loads issued before the sum)
-    const int rows = TC_BM / S, r0 = blockIdx.z * rows;
+    // CTA z reduces rows [z*128/SC, (z+1)*128/SC) over DSMEM in segment order
+    // seg_0 + seg_1 + ... (segment g lives in CTA g / G, partial g % G): the
+    // same order as the in-CTA path, one float4 per thread per pass
+    const int rows = TC_BM / SC, r0 = zc * rows;
     const int chunks = rows * (BN / 4);
     for (int idx = threadIdx.x; idx < chunks; idx += TC_THREADS) {
       const int r = r0 + idx / (BN / 4), c = (idx % (BN / 4)) * 4;
+      const float* src = part + r * PST + c;
       float4 a[8];
+      if (G == 1) {  // one segment per CTA: segment sg is CTA sg's only partial
 #pragma unroll
-      for (int s = 0; s < 8; ++s)
-        if (s < S) a[s] = ld_dsmem_f4(part + r * PST + c, (uint32_t)s);
+        for (int sg = 0; sg < 8; ++sg)
+          if (sg < S) a[sg] = ld_dsmem_f4(src, (uint32_t)(cx + CN * sg));
+      } else {
+#pragma unroll
+        for (int sg = 0; sg < 8; ++sg)
+          if (sg < S) a[sg] = ld_dsmem_f4(src + (sg % G) * PTILE, (uint32_t)(cx + CN * (sg / G)));
+      }
       float v[4] = {a[0].x, a[0].y, a[0].z, a[0].w};
 #pragma unroll
-      for (int s = 1; s < 8; ++s)
-        if (s < S) {
-          v[0] += a[s].x; v[1] += a[s].y; v[2] += a[s].z; v[3] += a[s].w;
+      for (int sg = 1; sg < 8; ++sg)
+        if (sg < S) {
+          v[0] += a[sg].x; v[1] += a[sg].y; v[2] += a[sg].z; v[3] += a[sg].w;
         }
       if (m0 + r < M && n0 + c < N) epi_store4(e, m0 + r, n0 + c, N, v);
     }
@@ -417,5 +486,7 @@ int tc_gemm(const TcWeights& w, int layer, const TcOperand& A, int M, int N, int
 void tc_release(TcWeights& w, TcActs& acts);
 // 2-D K-major TMA map: dims {K, rows}, box {128 B of K, box_rows}, 128 B swizzle
 int tc_make_map(CUtensorMap* m, const void* base, int esz, int K, int rows, int box_rows);
+// the A operand's maps (op.rows x op.cols at op.bf16 / op.hi+op.lo), every multicast width
+int tc_operand_maps(TcOperand& op, int precision);
 // standalone test entry (C-ABI wrapper in gemm_tc.cu)
 }  // namespace ps

@@ -339,7 +339,7 @@ int ps_unet_create(const ps_unet_config* cfg, const ps_dit_weights* w, ps_unet**
     s.A.rows = rows;
     s.A.cols = s.K;
     s.A.bf16 = op.pre == PRE_NONE ? (__nv_bfloat16*)h->bufs[op.in1] : h->scratch;
-    if ((rc = tc_make_map(&s.A.map_main, s.A.bf16, 2, s.K, rows, TC_BM))) return bail(rc);
+    if ((rc = tc_operand_maps(s.A, 1))) return bail(rc);
   }
   gemv_set_attr<float>();
   gemv_set_attr<__nv_bfloat16>();

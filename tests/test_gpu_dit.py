@@ -156,7 +156,8 @@ def test_dit_run_deterministic_and_graph():
     assert lanes.bitwise_equal(a)
 
 
-@pytest.mark.parametrize("shape", [(256, 1152, 1152), (256, 384, 1536), (256, 1152, 4608)])
+@pytest.mark.parametrize("shape", [(256, 1152, 1152), (256, 384, 1536), (256, 1152, 4608),
+                                   (256, 384, 384), (512, 1152, 384)])
 @pytest.mark.parametrize("precision", [0, 1])
 def test_gemm_split_paths_bitwise(shape, precision):
     """K segments as a DSMEM cluster (small M) and in one CTA (large M) must
@@ -168,4 +169,6 @@ def test_gemm_split_paths_bitwise(shape, precision):
     bias = torch.randn(N, device="cuda", generator=g)
     c_cluster = _gemm(A, W, bias, precision, 2)
     c_in_cta = _gemm(A, W, bias, precision, 3)
+    c_hybrid = _gemm(A, W, bias, precision, 4)  # 2 cluster CTAs x S/2 segments each
     assert torch.equal(c_cluster, c_in_cta)
+    assert torch.equal(c_cluster, c_hybrid)

@@ -14,21 +14,28 @@ int fmha_make_map(CUtensorMap* m, const __nv_bfloat16* qkv_bf16, int rows, int c
   return tc_make_map(m, qkv_bf16, 2, cols, rows, FM_BK);
 }
 
-template <int DH>
+template <int DH, int NQ>
 static cudaError_t fmha_go(const CUtensorMap& map, const FmhaArgs& a, cudaStream_t st) {
+  using C = FmCfg<DH, NQ>;
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(fmha_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         FmCfg<DH>::SMEM);
+    cudaFuncSetAttribute(fmha_tc_kernel<DH, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         C::SMEM);
   });
-  return launch_pdl(fmha_tc_kernel<DH>, dim3((a.L + FM_BQ - 1) / FM_BQ, a.H, a.B),
-                    dim3(FM_THREADS), FmCfg<DH>::SMEM, st, map, a);
+  return launch_pdl(fmha_tc_kernel<DH, NQ>, dim3((a.L + NQ * FM_BQ - 1) / (NQ * FM_BQ), a.H, a.B),
+                    dim3(C::THREADS), C::SMEM, st, map, a);
 }
+
+static int g_fmha_nq = 0;  // test hook: force 1 or 2 query tiles per CTA (0 = auto)
 
 int fmha_launch(const CUtensorMap& map, const FmhaArgs& a, cudaStream_t st) {
   const int DH = fmha_padded_dim(a.dh);
   if (DH == 0) return fail(PS_EUNSUP, "tcgen05 attention: head_dim must be a multiple of 8, <= 128");
-  cudaError_t e = DH == 64 ? fmha_go<64>(map, a, st) : fmha_go<128>(map, a, st);
+  // two query tiles per CTA once the grid has enough CTAs for the SMs
+  const int ctas1 = (a.L + FM_BQ - 1) / FM_BQ * a.H * a.B;
+  const bool two = DH == 64 && (g_fmha_nq == 2 || (g_fmha_nq == 0 && ctas1 >= 4 * 148));
+  cudaError_t e = DH == 128 ? fmha_go<128, 1>(map, a, st)
+                            : (two ? fmha_go<64, 2>(map, a, st) : fmha_go<64, 1>(map, a, st));
   if (e != cudaSuccess) return fail((int)e, std::string("fmha: ") + cudaGetErrorString(e));
   return check_launch("fmha");
 }
@@ -137,16 +144,20 @@ extern "C" {
 
 int ps_attn_test(const float* qkv, float* out, int B, int L, int H, int D, int impl, void* cs) {
   PS_CHECK_ARG(qkv && out && B >= 1 && L >= 1 && H >= 1 && D % H == 0, "bad attention arguments");
-  PS_CHECK_ARG(impl == 1 || impl == 2, "impl must be 1 (mma.sync) or 2 (tcgen05)");
+  PS_CHECK_ARG(impl >= 1 && impl <= 4, "impl: 1 mma.sync, 2 tcgen05 (auto), 3/4 tcgen05 1/2 tiles");
   int rc = 0;
-  attn_run(qkv, out, B, L, H, D, impl, 0, as_stream(cs), &rc);
+  g_fmha_nq = impl == 3 ? 1 : (impl == 4 ? 2 : 0);
+  attn_run(qkv, out, B, L, H, D, impl >= 2 ? 2 : 1, 0, as_stream(cs), &rc);
+  g_fmha_nq = 0;
   return rc;
 }
 
 float ps_attn_probe(int B, int L, int H, int D, int impl, int iters) {
-  if (B < 1 || L < 1 || H < 1 || D % H || iters < 1) return -1.f;
+  if (B < 1 || L < 1 || H < 1 || D % H || iters < 1 || impl < 1 || impl > 4) return -1.f;
   int rc = 0;
-  float us = attn_run(nullptr, nullptr, B, L, H, D, impl, iters, 0, &rc);
+  g_fmha_nq = impl == 3 ? 1 : (impl == 4 ? 2 : 0);
+  float us = attn_run(nullptr, nullptr, B, L, H, D, impl >= 2 ? 2 : 1, iters, 0, &rc);
+  g_fmha_nq = 0;
   return rc ? -1.f : us;
 }
 

@@ -28,21 +28,28 @@
 namespace ps {
 
 constexpr int FM_BQ = 128, FM_BK = 128;
-constexpr int FM_THREADS = 192;
 constexpr int FM_TILE = 128 * 128;  // bytes of one 128-row x 128-byte (64 bf16) box
 
 // DH = padded head width in smem/TMEM (64, or 128 for head_dim 72..128):
 // NA = DH/64 swizzle atoms along the head dim per Q/K/V tile.
-template <int DH>
+// NQ = 128-query tiles per CTA sharing each K/V block:
+//   NQ = 1: S double-buffered in TMEM (S0 [0,128) S1 [128,256), O [256,256+DH)),
+//           P double-buffered in smem; short sequences (more CTAs)
+//   NQ = 2: two softmax warpgroups ping-pong (tile t: S_t [128t, 128t+128),
+//           O_t [256 + 64t, ...)), one S and one P buffer per tile; the tensor
+//           core runs tile 1's MMAs under tile 0's softmax and vice versa
+template <int DH, int NQ>
 struct FmCfg {
   static constexpr int NA = DH / 64;
   static constexpr int STAGES = DH == 64 ? 3 : 2;
+  static constexpr int THREADS = (4 * NQ + 2) * 32;
   static constexpr int Q_OFF = 0;
-  static constexpr int KV_OFF = NA * FM_TILE;  // stage s: K at +2s*NA*TILE, V at +(2s+1)*NA*TILE
+  static constexpr int KV_OFF = NQ * NA * FM_TILE;  // stage s: K at +2s*NA*TILE, V at +(2s+1)*NA*TILE
   static constexpr int P_OFF = KV_OFF + 2 * STAGES * NA * FM_TILE;  // 2 buffers x 2 key atoms
   static constexpr int BAR_OFF = P_OFF + 4 * FM_TILE;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
-  static constexpr uint32_t TMEM_COLS = 512;  // S0 [0,128) S1 [128,256) O [256, 256+DH)
+  static constexpr uint32_t TMEM_COLS = 512;
+  static_assert(NQ == 1 || DH == 64, "two query tiles only for 64-wide heads (smem)");
 };
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
@@ -86,10 +93,11 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
-template <int DH>
-__global__ void __launch_bounds__(FM_THREADS, 1)
+template <int DH, int NQ>
+__global__ void __launch_bounds__(FmCfg<DH, NQ>::THREADS, 1)
     fmha_tc_kernel(const __grid_constant__ CUtensorMap mapQKV, const __grid_constant__ FmhaArgs p) {
-  using C = FmCfg<DH>;
+  using C = FmCfg<DH, NQ>;
+  constexpr int W_TMA = 4 * NQ, W_MMA = 4 * NQ + 1;
   constexpr int NA = C::NA, FM_STAGES = C::STAGES, FM_Q_OFF = C::Q_OFF, FM_KV_OFF = C::KV_OFF,
                 FM_P_OFF = C::P_OFF, FM_BAR_OFF = C::BAR_OFF;
   constexpr uint32_t FM_TMEM_COLS = C::TMEM_COLS;
@@ -106,7 +114,7 @@ __global__ void __launch_bounds__(FM_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int q0 = blockIdx.x * FM_BQ, head = blockIdx.y, b = blockIdx.z;
+  const int q0 = blockIdx.x * FM_BQ * NQ, head = blockIdx.y, b = blockIdx.z;
   const int L = p.L;
   const int nkb = (L + FM_BK - 1) / FM_BK;
   const int row_base = b * L;
@@ -118,7 +126,7 @@ __global__ void __launch_bounds__(FM_THREADS, 1)
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 2; ++i) {  // NQ = 1: buffer j & 1; NQ = 2: query tile
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 128);
       mbar_init(&pv_done[i], 1);
@@ -135,18 +143,18 @@ __global__ void __launch_bounds__(FM_THREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS[2] = {tmem, tmem + 128};
-  const uint32_t tO = tmem + 256;
   pdl_wait_and_release();
 
-  if (warp == 4) {
+  if (warp == W_TMA) {
     if (lane == 0) {
       // ---------------- TMA producer
       // column of (which, head, atom a) in the [rows, 3*H*DH] operand
       const int hc = head * DH, wstride = p.H * DH;
-      mbar_expect_tx(q_full, NA * FM_TILE);
-      for (int a = 0; a < NA; ++a)
-        tma_load_2d(smem + FM_Q_OFF + a * FM_TILE, &mapQKV, q_full, hc + 64 * a, row_base + q0);
+      mbar_expect_tx(q_full, NQ * NA * FM_TILE);
+      for (int t = 0; t < NQ; ++t)
+        for (int a = 0; a < NA; ++a)
+          tma_load_2d(smem + FM_Q_OFF + (t * NA + a) * FM_TILE, &mapQKV, q_full, hc + 64 * a,
+                      row_base + q0 + t * FM_BQ);
       for (int j = 0; j < nkb; ++j) {
         const int s = j % FM_STAGES;
         mbar_wait(&kv_empty[s], ((j / FM_STAGES) & 1) ^ 1);
@@ -160,69 +168,111 @@ __global__ void __launch_bounds__(FM_THREADS, 1)
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == W_MMA) {
     if (lane == 0) {
       // ---------------- MMA issuer
       constexpr uint32_t idS = make_idesc(KIND_BF16, 128, 128);
       constexpr uint32_t idPV = make_idesc(KIND_BF16, 128, DH) | (1u << 16);  // B (V) MN-major
-      auto issue_s = [&](int j) {
+      // S_t(j) = Q_t K_j^T into S buffer `sb`
+      auto issue_s = [&](int t, int j, int sb) {
         const int s = j % FM_STAGES;
         mbar_wait(&kv_full[s], (j / FM_STAGES) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint8_t* kt = smem + FM_KV_OFF + 2 * s * NA * FM_TILE;
+        const uint8_t* qt = smem + FM_Q_OFF + t * NA * FM_TILE;
 #pragma unroll
         for (int k = 0; k < DH / 16; ++k) {  // atom k/4, +32 B along K inside it
-          const uint64_t qd = smem_desc_sw128(smem + FM_Q_OFF + (k >> 2) * FM_TILE) + 2 * (k & 3);
+          const uint64_t qd = smem_desc_sw128(qt + (k >> 2) * FM_TILE) + 2 * (k & 3);
           const uint64_t kd = smem_desc_sw128(kt + (k >> 2) * FM_TILE) + 2 * (k & 3);
-          umma<KIND_BF16>(tS[j & 1], qd, kd, idS, k > 0 ? 1u : 0u);
+          umma<KIND_BF16>(tmem + 128 * sb, qd, kd, idS, k > 0 ? 1u : 0u);
         }
-        umma_commit(&s_full[j & 1]);
+        umma_commit(&s_full[sb]);
       };
-      mbar_wait(q_full, 0);
-      issue_s(0);
-      if (nkb > 1) issue_s(1);
-      for (int j = 0; j < nkb; ++j) {
-        mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+      // O_t += P(buffer pb) V_j, once P has been written (p_full[pb], parity par)
+      auto issue_pv = [&](int t, int j, int pb, int par) {
+        mbar_wait(&p_full[pb], par);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const int s = j % FM_STAGES;
-        const uint8_t* pb = smem + FM_P_OFF + (j & 1) * 2 * FM_TILE;
+        const uint8_t* pbuf = smem + FM_P_OFF + pb * 2 * FM_TILE;
         // V: MN-major, NA atoms of 64 dims at FM_TILE stride (LBO), 8-key groups at 1 KB (SBO)
         const uint64_t vd = (smem_desc_sw128(smem + FM_KV_OFF + (2 * s + 1) * NA * FM_TILE) &
                              ~(0x3FFFull << 16)) |
                             ((uint64_t)(FM_TILE >> 4) << 16);
+        const uint32_t tO = tmem + 256 + (NQ == 1 ? 0 : t * DH);
 #pragma unroll
         for (int k = 0; k < FM_BK / 16; ++k) {
           // P: K-major, keys [64a, 64a+64) in atom column a; V: MN-major, 16 keys = 2048 B
-          const uint64_t pd = smem_desc_sw128(pb + (k >> 2) * FM_TILE) + 2 * (k & 3);
+          const uint64_t pd = smem_desc_sw128(pbuf + (k >> 2) * FM_TILE) + 2 * (k & 3);
           umma<KIND_BF16>(tO, pd, vd + (uint64_t)(k * 2048 >> 4), idPV, (j | k) ? 1u : 0u);
         }
-        umma_commit(&kv_empty[s]);
-        umma_commit(&pv_done[j & 1]);
-        if (j + 2 < nkb) issue_s(j + 2);
+      };
+      mbar_wait(q_full, 0);
+      if constexpr (NQ == 1) {
+        issue_s(0, 0, 0);
+        if (nkb > 1) issue_s(0, 1, 1);
+        for (int j = 0; j < nkb; ++j) {
+          issue_pv(0, j, j & 1, (j >> 1) & 1);
+          umma_commit(&kv_empty[j % FM_STAGES]);
+          umma_commit(&pv_done[j & 1]);
+          if (j + 2 < nkb) issue_s(0, j + 2, j & 1);
+        }
+      } else {
+        issue_s(0, 0, 0);
+        issue_s(1, 0, 1);
+        for (int j = 0; j < nkb; ++j) {
+          issue_pv(0, j, 0, j & 1);
+          umma_commit(&pv_done[0]);
+          if (j + 1 < nkb) issue_s(0, j + 1, 0);  // tile 0's next scores under tile 1's softmax
+          issue_pv(1, j, 1, j & 1);
+          umma_commit(&kv_empty[j % FM_STAGES]);
+          umma_commit(&pv_done[1]);
+          if (j + 1 < nkb) issue_s(1, j + 1, 1);
+        }
       }
     }
   } else {
-    // ---------------- softmax warps: thread r <-> query row r <-> TMEM lane r
-    const int r = threadIdx.x;  // 0..127
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    // ---------------- softmax warps: tile t, thread r <-> query row r <-> TMEM lane r
+    const int t = warp >> 2;
+    const int r = threadIdx.x & 127;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t tO = tmem + 256 + (NQ == 1 ? 0 : t * DH);
+    // NQ = 1: buffers alternate per block (phase per pair of blocks);
+    // NQ = 2: one buffer per tile (phase per block)
+    auto buf = [&](int j) { return NQ == 1 ? (j & 1) : t; };
+    auto par = [&](int j) { return NQ == 1 ? ((j >> 1) & 1) : (j & 1); };
     const float sl2 = p.scale_log2;
     float m_ref = -INFINITY, l = 0.f;
     for (int j = 0; j < nkb; ++j) {
-      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      mbar_wait(&s_full[buf(j)], par(j));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      float s[FM_BK];
-#pragma unroll
-      for (int c = 0; c < FM_BK / 32; ++c) tmem_ld32(tS[j & 1] + lane_off + c * 32, s + c * 32);
-      tmem_ld_wait();
+      // Row max. NQ = 1: the whole 128-column S row is loaded once and kept in
+      // registers for the exp pass; NQ = 2 (register-limited, 10 warps):
+      // streamed from TMEM 64 columns at a time and reloaded for the exp pass.
+      // Reductions use 8 independent partial maxima / 4 partial sums (no
+      // 128-long dependency chain); the order is fixed, so results do not
+      // depend on NQ.
+      const uint32_t srow = tmem + 128 * buf(j) + lane_off;
       const int valid = L - j * FM_BK;  // keys of this block inside the lane
-      if (valid < FM_BK) {
+      constexpr int CH = NQ == 1 ? FM_BK : 64;  // columns per TMEM load group
+      float sv[CH];
+      float pm[8];
 #pragma unroll
-        for (int c = 0; c < FM_BK; ++c)
-          if (c >= valid) s[c] = -INFINITY;
+      for (int i = 0; i < 8; ++i) pm[i] = -INFINITY;
+#pragma unroll
+      for (int g = 0; g < FM_BK / CH; ++g) {
+#pragma unroll
+        for (int c = 0; c < CH / 32; ++c) tmem_ld32(srow + g * CH + c * 32, sv + c * 32);
+        tmem_ld_wait();
+        if (valid < FM_BK) {  // last block only: keys past the lane -> -inf (p = 0)
+#pragma unroll
+          for (int i = 0; i < CH; ++i)
+            if (g * CH + i >= valid) sv[i] = -INFINITY;
+        }
+#pragma unroll
+        for (int i = 0; i < CH; ++i) pm[i & 7] = fmaxf(pm[i & 7], sv[i]);
       }
-      float mx = s[0];
-#pragma unroll
-      for (int c = 1; c < FM_BK; ++c) mx = fmaxf(mx, s[c]);
+      const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
+                             fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
       const float m_new = mx * sl2;
       if (j == 0) {
         m_ref = m_new;
@@ -230,7 +280,7 @@ __global__ void __launch_bounds__(FM_THREADS, 1)
         const bool need = m_new > m_ref + 8.f;
         if (__any_sync(0xffffffffu, need)) {
           // O's row must hold P_{j-1} V_{j-1} before it is rescaled
-          mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+          mbar_wait(&pv_done[buf(j - 1)], par(j - 1));
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const float m_tgt = need ? m_new : m_ref;
           const float f = fast_exp2(m_ref - m_tgt);
@@ -248,35 +298,52 @@ __global__ void __launch_bounds__(FM_THREADS, 1)
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
       }
-      // P buffer (j & 1) was last read by P_{j-2} V_{j-2}
-      if (j >= 2) mbar_wait(&pv_done[j & 1], ((j - 2) >> 1) & 1);
-      uint8_t* prow = smem + FM_P_OFF + (j & 1) * 2 * FM_TILE + r * 128;
-      float rs = 0.f;
+      // the P buffer was last read by P V of block j-2 (NQ = 1) / j-1 (NQ = 2)
+      if (NQ == 1 && j >= 2) mbar_wait(&pv_done[buf(j)], par(j - 2));
+      if (NQ == 2 && j >= 1) mbar_wait(&pv_done[t], par(j - 1));
+      uint8_t* prow = smem + FM_P_OFF + buf(j) * 2 * FM_TILE + r * 128;
+      float ps[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int kc = 0; kc < FM_BK / 8; ++kc) {  // 16-byte chunks of 8 keys
-        uint32_t u[4];
+      for (int g = 0; g < FM_BK / CH; ++g) {  // exp2, row sum, bf16 P row
+        if (NQ != 1) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float p0 = fast_exp2(fmaf(s[kc * 8 + 2 * q], sl2, -m_ref));
-          const float p1 = fast_exp2(fmaf(s[kc * 8 + 2 * q + 1], sl2, -m_ref));
-          rs += p0 + p1;
-          u[q] = pack_bf16(p0, p1);
+          for (int c = 0; c < CH / 32; ++c) tmem_ld32(srow + g * CH + c * 32, sv + c * 32);
+          tmem_ld_wait();
+          if (valid < FM_BK) {
+#pragma unroll
+            for (int i = 0; i < CH; ++i)
+              if (g * CH + i >= valid) sv[i] = -INFINITY;
+          }
         }
-        const int a = kc >> 3, c = kc & 7;
-        *reinterpret_cast<uint4*>(prow + a * FM_TILE + ((c ^ (r & 7)) << 4)) =
-            make_uint4(u[0], u[1], u[2], u[3]);
+#pragma unroll
+        for (int h = 0; h < CH / 8; ++h) {  // 16-byte chunk of 8 keys
+          uint32_t u[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int i0 = h * 8 + 2 * q;  // masked keys hold -inf: exp2 -> +0
+            const float p0 = fast_exp2(fmaf(sv[i0], sl2, -m_ref));
+            const float p1 = fast_exp2(fmaf(sv[i0 + 1], sl2, -m_ref));
+            ps[q] += p0 + p1;
+            u[q] = pack_bf16(p0, p1);
+          }
+          const int kc = g * (CH / 8) + h, a = kc >> 3, cc = kc & 7;
+          *reinterpret_cast<uint4*>(prow + a * FM_TILE + ((cc ^ (r & 7)) << 4)) =
+              make_uint4(u[0], u[1], u[2], u[3]);
+        }
       }
+      const float rs = (ps[0] + ps[1]) + (ps[2] + ps[3]);
       l += rs;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mbar_arrive(&p_full[j & 1]);
+      mbar_arrive(&p_full[buf(j)]);
     }
     // ---------------- epilogue: O / l -> bf16 [B*L, D]
-    mbar_wait(&pv_done[(nkb - 1) & 1], ((nkb - 1) >> 1) & 1);
+    mbar_wait(&pv_done[buf(nkb - 1)], par(nkb - 1));
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const float inv = 1.f / l;
-    const bool ok = q0 + r < L;
-    __nv_bfloat16* orow = p.out_bf16 + (int64_t)(row_base + q0 + r) * p.D + head * p.dh;
+    const int q = q0 + t * FM_BQ + r;
+    const bool ok = q < L;
+    __nv_bfloat16* orow = p.out_bf16 + (int64_t)(row_base + q) * p.D + head * p.dh;
 #pragma unroll
     for (int c = 0; c < DH / 32; ++c) {
       float o[32];

@@ -16,7 +16,7 @@ SHAPES = [("cogvideox_2b", 1, 17550, 30, 1920), ("dit_s2 bf16 L=256", 1, 256, 6,
 print(f"{'shape':24s} {'impl':>4s} {'us':>10s} {'TFLOP/s':>8s}")
 for name, B, L, H, D in SHAPES:
     flops = 4.0 * B * L * L * D
-    for impl in (1, 2):
+    for impl in (1, 3, 4):  # mma.sync, tcgen05 with 1 / 2 query tiles per CTA
         iters = 3 if L > 10000 else 20
         us = lib.ps_attn_probe(B, L, H, D, impl, iters)
         tf = flops / (us * 1e-6) / 1e12 if us > 0 else float("nan")

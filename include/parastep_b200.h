@@ -163,11 +163,15 @@ int ps_gemm_test(const float* A, const float* W, const float* bias, float* C, in
 float ps_gemm_probe(int M, int N, int K, int precision, int dbg, int iters);
 /* Diagnostic: clock64 phase stamps of CTA (0,0,0) of the last probe launch
  * run with dbg bit 4 (entry, prologue, PDL wait, first TMA, first stage,
- * last stage, accumulator ready, epilogue done, exit). */
-int ps_gemm_stamps(long long* out9);
+ * last stage, accumulator ready, epilogue done, exit; split-K: partials
+ * written, first cluster sync, reduction done). */
+int ps_gemm_stamps(long long* out12);
 /* Tuning knob: minimum K-blocks per split-K segment for layers prepared
  * afterwards (default 4); returns the previous value. */
 int ps_gemm_tune(int split_min_kb);
+/* Calibration: force the planned N-tile width / split-K of layers prepared
+ * afterwards (0 = the planner's choice). */
+void ps_gemm_force(int bn, int splits);
 
 /* ---- U-Net-shaped predictor (paper_2505_14741_b200/unet_spec.py) -------
  * A native executor for the op list unet_spec.plan() emits (bf16 tcgen05

@@ -89,6 +89,7 @@ _SIGS = {
     "ps_dit_bench_gemm": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]),
     "ps_gemm_stamps": (C.c_int, [C.POINTER(C.c_longlong)]),
     "ps_gemm_tune": (C.c_int, [C.c_int]),
+    "ps_gemm_force": (None, [C.c_int, C.c_int]),
     "ps_gemm_probe": (C.c_float, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
     "ps_unet_create": (C.c_int, [C.POINTER(ps_unet_config), C.POINTER(ps_dit_weights),
                                  C.POINTER(C.c_void_p)]),

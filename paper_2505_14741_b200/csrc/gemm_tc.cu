@@ -181,43 +181,47 @@ static int launch(const TcLayer& L, const TcOperand& A, int M, int N, int K, con
 // (ref_rows), so a row's accumulation order never depends on the batch
 // (forward_batch == mapped forward, bitwise); BN may change per call.
 static int g_split_min_kb = 2;  // ps_gemm_tune: K-blocks each split keeps at least (tf3x)
+static int g_force_bn = 0, g_force_splits = 0;  // ps_gemm_force (calibration only)
 
 
 struct TilePlan {
   int bn, splits;
 };
 
-// bf16 (2 B/element): ingest matters less than the DSMEM reduction, which
-// measured slower than modelled; the narrow-tile policy below wins there:
-// split while the grid (64-wide tiles) stays co-resident and each split keeps
-// >= 4 K-blocks, then 32-wide tiles when the grid covers <= half the SMs.
-static TilePlan plan_tiles_bf16(int M, int N, int K) {
-  const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + 63) / 64);
-  const int nk = (K + 63) / 64;
-  int s = 1;
-  while (s < 8 && tiles * s * 2 <= cluster_cap(s * 2) && nk / (s * 2) >= 4) s *= 2;
-  if (!g_split_enable) s = 1;
-  return TilePlan{2 * tiles * s <= cluster_cap(s) ? 32 : 64, s};
-}
+static TilePlan plan_tiles_auto(int precision, int M, int N, int K);
 
 static TilePlan plan_tiles(int precision, int M, int N, int K) {
-  if (precision == 1) return plan_tiles_bf16(M, N, K);
+  TilePlan p = plan_tiles_auto(precision, M, N, K);
+  if (g_force_bn) p.bn = g_force_bn;
+  if (g_force_splits) p.splits = g_force_splits;
+  return p;
+}
+
+// Cost model fitted to the (BN, S) calibration grid (profiles/r1b_gemm_plan_grid.txt,
+// tools/gemm_plan_grid.py), in microseconds per launch:
+//   mainloop  = per-CTA operand ingest / 70 GB/s (per-SM TMA ingest)
+//   split-K   = 1.3 (two cluster barriers) + the CTA's share of the DSMEM
+//               reduction, 128 x BN x 4 B x (S-1)/S at ~25 GB/s
+//   no split  = 0.3 (plain epilogue)
+// (BN = 128, S = 8) measured far off the model (cluster placement) and is
+// excluded. Grids beyond one wave pay per wave.
+static TilePlan plan_tiles_auto(int precision, int M, int N, int K) {
   const int bk = precision == 1 ? 64 : 32;       // K elements per 128-byte stage row
   const double esz = precision == 1 ? 2.0 : 8.0;  // bytes per element incl. the tf32 lo copy
   const int nk = (K + bk - 1) / bk, tm = (M + TC_BM - 1) / TC_BM;
   TilePlan best{64, 1};
   double best_cost = 1e300;
-  const int bns[3] = {128, 64, 32};
+  const int bns[3] = {32, 64, 128};
   for (int bn : bns) {
     const int tn = (N + bn - 1) / bn;
     for (int s = 1; s <= 8; s *= 2) {
       if (s > 1 && (tm * tn * s > cluster_cap(s) || nk / s < g_split_min_kb)) break;
-      const int ctas = tm * tn * s;
-      const int waves = (ctas + 147) / 148;
-      double cost = waves * ((double)((nk + s - 1) / s) * bk * (128 + bn) * esz);
-      if (s > 1) cost += 128.0 * bn * 4 + 40e3;  // DSMEM partial tile + 2 cluster syncs
-      if (cost < best_cost * 0.97) {  // prefer the earlier (wider / fewer-split) plan on ties
-        best_cost = cost;
+      if (bn == 128 && s == 8) break;
+      const int waves = (tm * tn * s + 147) / 148;
+      double us = waves * ((double)((nk + s - 1) / s) * bk * (128 + bn) * esz / 70e3);
+      us += s > 1 ? 1.3 + 128.0 * bn * 4 * (s - 1) / s / 25e3 : 0.3;
+      if (us < best_cost * 0.98) {  // ties: the narrower / fewer-split plan
+        best_cost = us;
         best = TilePlan{bn, s};
       }
     }
@@ -439,6 +443,13 @@ float ps_gemm_probe(int M, int N, int K, int precision, int dbg, int iters) {
 
 // Tuning knob (diagnostic): minimum K-blocks per split-K segment; affects
 // layers prepared afterwards. Returns the previous value.
+// Calibration: force the planned (BN, S) of layers prepared afterwards
+// (0 = planner's choice).
+void ps_gemm_force(int bn, int splits) {
+  g_force_bn = bn;
+  g_force_splits = splits;
+}
+
 int ps_gemm_tune(int split_min_kb) {
   const int prev = g_split_min_kb;
   if (split_min_kb >= 1) g_split_min_kb = split_min_kb;
@@ -449,11 +460,11 @@ int ps_gemm_tune(int split_min_kb) {
 // with dbg bit 4 set: [entry, prologue done, PDL wait done, first TMA
 // issued, first stage landed (MMA), last stage landed, accumulator ready,
 // epilogue done, exit].
-int ps_gemm_stamps(long long* out9) {
+int ps_gemm_stamps(long long* out12) {
   long long h[16];
   cudaError_t e = cudaMemcpyFromSymbol(h, g_tc_ts, sizeof(h));
   if (e != cudaSuccess) return fail((int)e, "stamps");
-  for (int i = 0; i < 9; ++i) out9[i] = h[i];
+  for (int i = 0; i < 12; ++i) out12[i] = h[i];
   return 0;
 }
 

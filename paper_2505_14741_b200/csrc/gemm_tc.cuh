@@ -229,16 +229,17 @@ struct TcSplit {
 };
 // cluster dims (cn, 1, cluster): rank = x + cn * z
 
+// DSMEM load of a peer's partial tile. Not volatile / no memory clobber: the
+// data is immutable between the two cluster barriers that bracket the
+// reduction (those carry the ordering), so the compiler may batch and
+// hoist these loads across iterations.
 __device__ __forceinline__ float4 ld_dsmem_f4(const float* local, uint32_t cta) {
   uint32_t remote;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
-               : "=r"(remote)
-               : "r"(smem_u32(local)), "r"(cta));
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(cta));
   float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(remote)
-               : "memory");
+  asm("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "r"(remote));
   return v;
 }
 
@@ -434,33 +435,44 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         *reinterpret_cast<float4*>(dst + 4 * q) =
             make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     }
+    if (threadIdx.x == 0) TC_STAMP(9);
     cluster_sync_all();
+    if (threadIdx.x == 0) TC_STAMP(10);
     // CTA z reduces rows [z*128/SC, (z+1)*128/SC) over DSMEM in segment order
     // seg_0 + seg_1 + ... (segment g lives in CTA g / G, partial g % G): the
     // same order as the in-CTA path, one float4 per thread per pass
     const int rows = TC_BM / SC, r0 = zc * rows;
     const int chunks = rows * (BN / 4);
-    for (int idx = threadIdx.x; idx < chunks; idx += TC_THREADS) {
-      const int r = r0 + idx / (BN / 4), c = (idx % (BN / 4)) * 4;
-      const float* src = part + r * PST + c;
-      float4 a[8];
-      if (G == 1) {  // one segment per CTA: segment sg is CTA sg's only partial
+    // two float4 chunks per thread per pass: 2 x S remote loads in flight
+    for (int base = threadIdx.x; base < chunks; base += 2 * TC_THREADS) {
+      float4 a[2][8];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int idx = base + u * TC_THREADS;
+        if (idx >= chunks) break;
+        const int r = r0 + idx / (BN / 4), c = (idx % (BN / 4)) * 4;
+        const float* src = part + r * PST + c;
 #pragma unroll
         for (int sg = 0; sg < 8; ++sg)
-          if (sg < S) a[sg] = ld_dsmem_f4(src, (uint32_t)(cx + CN * sg));
-      } else {
-#pragma unroll
-        for (int sg = 0; sg < 8; ++sg)
-          if (sg < S) a[sg] = ld_dsmem_f4(src + (sg % G) * PTILE, (uint32_t)(cx + CN * (sg / G)));
+          if (sg < S)
+            a[u][sg] = G == 1 ? ld_dsmem_f4(src, (uint32_t)(cx + CN * sg))
+                              : ld_dsmem_f4(src + (sg % G) * PTILE, (uint32_t)(cx + CN * (sg / G)));
       }
-      float v[4] = {a[0].x, a[0].y, a[0].z, a[0].w};
 #pragma unroll
-      for (int sg = 1; sg < 8; ++sg)
-        if (sg < S) {
-          v[0] += a[sg].x; v[1] += a[sg].y; v[2] += a[sg].z; v[3] += a[sg].w;
-        }
-      if (m0 + r < M && n0 + c < N) epi_store4(e, m0 + r, n0 + c, N, v);
+      for (int u = 0; u < 2; ++u) {
+        const int idx = base + u * TC_THREADS;
+        if (idx >= chunks) break;
+        const int r = r0 + idx / (BN / 4), c = (idx % (BN / 4)) * 4;
+        float v[4] = {a[u][0].x, a[u][0].y, a[u][0].z, a[u][0].w};
+#pragma unroll
+        for (int sg = 1; sg < 8; ++sg)
+          if (sg < S) {
+            v[0] += a[u][sg].x; v[1] += a[u][sg].y; v[2] += a[u][sg].z; v[3] += a[u][sg].w;
+          }
+        if (m0 + r < M && n0 + c < N) epi_store4(e, m0 + r, n0 + c, N, v);
+      }
     }
+    if (threadIdx.x == 0) TC_STAMP(11);
     cluster_sync_all();  // peers' smem stays live until every CTA has read it
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

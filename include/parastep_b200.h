@@ -213,6 +213,22 @@ int ps_unet_forward(ps_unet* h, const float* x, const int32_t* host_ts, int B, f
 int ps_unet_destroy(ps_unet* h);
 int ps_unet_kernels_per_forward(const ps_unet* h);
 
+/* ---- trajectory files and diagnostics on device --------
+ * ps_traj_pack writes the reference's binary trajectory file
+ * (trajectory_io.py:100-110, "PSTJ" v1, little-endian float64 payload) into
+ * `out` (ps_traj_pack_bytes(T, n) bytes) from device tables: rec_x [T][n],
+ * eps rows eps[src_row[k]], x0 [n]; ts / fresh / src_row are device arrays.
+ * ps_traj_diff writes out[r] = {sum|a-b|, sum|a|, sum (a-b)^2} (fp64, fixed
+ * order) of row rows_a[r] of a against row rows_b[r] of b (null = identity):
+ * the sums behind rel_mae / mse / compare_trajectories (numerics.py:144-158,
+ * engines.py:446-473). */
+int64_t ps_traj_pack_bytes(int T, int64_t n);
+int ps_traj_pack(const void* rec_x, const void* eps, const void* x0, const int32_t* src_row,
+                 const int32_t* ts, const uint8_t* fresh, int T, int64_t n, int dtype, void* out,
+                 void* cuda_stream);
+int ps_traj_diff(const void* a, const void* b, const int32_t* rows_a, const int32_t* rows_b,
+                 int rows, int64_t n, int dtype_a, int dtype_b, double* out, void* cuda_stream);
+
 /* Diagnostic (allocates + synchronises): softmax(Q K^T / sqrt(dh)) V over
  * qkv fp32 [B*L, 3D] (row m = [q | k | v], heads of dh = D/H contiguous)
  * into out fp32 [B*L, D], operands rounded to bf16: impl 1 = mma.sync flash

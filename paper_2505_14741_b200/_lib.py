@@ -97,6 +97,11 @@ _SIGS = {
                                   C.c_void_p, C.c_void_p]),
     "ps_unet_destroy": (C.c_int, [C.c_void_p]),
     "ps_unet_kernels_per_forward": (C.c_int, [C.c_void_p]),
+    "ps_traj_pack_bytes": (C.c_int64, [C.c_int, C.c_int64]),
+    "ps_traj_pack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                               C.c_void_p, C.c_int, C.c_int64, C.c_int, C.c_void_p, C.c_void_p]),
+    "ps_traj_diff": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                               C.c_int64, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
     "ps_attn_test": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
                                C.c_int, C.c_void_p]),
     "ps_attn_probe": (C.c_float, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),

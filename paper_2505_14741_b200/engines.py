@@ -397,6 +397,13 @@ class DeviceSampler:
         self.run(seed, graph=graph, x_init=x_init)
         return self.trajectory()
 
+    def save_trajectory_binary(self, path) -> None:
+        """The reference's binary trajectory file of the last run, packed on device."""
+        from .trajectory_io import pack_device
+
+        with open(path, "wb") as fh:
+            fh.write(pack_device(self))
+
     def trajectory(self) -> Trajectory:
         """Copy the run's records to host (reference Trajectory of float64 vectors)."""
         import torch
@@ -581,3 +588,43 @@ def compare_trajectories(a: Trajectory, b: Trajectory):
         rows.append(DiffRow(ra.t, rel_mae(ra.x, rb.x), rel_mae(ra.eps, rb.eps), mse(ra.x, rb.x),
                             mse(ra.eps, rb.eps)))
     return rows, rel_mae(a.x0, b.x0)
+
+
+def compare_trajectories_device(a: "DeviceSampler", b: "DeviceSampler"):
+    """compare_trajectories of two samplers' last runs without leaving the GPU.
+
+    Same rows (t, rel-MAE / MSE of x and eps, a = reference) and final x0
+    rel-MAE as ``compare_trajectories`` (engines.py:446-473); the sums run on
+    device in fp64 with a fixed reduction order (``ps_traj_diff``), so they
+    agree with the host's left-to-right sums to rounding (~1e-15 relative).
+    """
+    import torch
+
+    if a.T != b.T or a.n != b.n:
+        raise DimensionError(f"trajectory shapes differ: {a.T}x{a.n} vs {b.T}x{b.n}")
+    if not (a.record and b.record):
+        raise ConfigError("both samplers need per-step x records")
+    lib = _lib.load(require_gpu=True)
+    T, n = a.T, a.n
+    out = torch.empty((2 * T + 1, 3), dtype=torch.float64, device="cuda")
+    ra = torch.tensor(a.src_row, dtype=torch.int32, device="cuda")
+    rb = torch.tensor(b.src_row, dtype=torch.int32, device="cuda")
+    st = _lib.stream_ptr()
+    _lib.check(lib.ps_traj_diff(_lib.ptr(a.rec_x), _lib.ptr(b.rec_x), None, None, T, n,
+                                a.dtype_code, b.dtype_code, _lib.ptr(out), st), "traj_diff")
+    _lib.check(lib.ps_traj_diff(_lib.ptr(a.eps), _lib.ptr(b.eps), _lib.ptr(ra), _lib.ptr(rb), T, n,
+                                a.dtype_code, b.dtype_code, _lib.ptr(out) + 3 * T * 8, st),
+               "traj_diff")
+    _lib.check(lib.ps_traj_diff(_lib.ptr(a.x0_device), _lib.ptr(b.x0_device), None, None, 1, n,
+                                a.dtype_code, b.dtype_code, _lib.ptr(out) + 6 * T * 8, st),
+               "traj_diff")
+    s = out.cpu().numpy()
+
+    def rel(row):
+        if row[1] == 0.0:
+            raise DegenerateReferenceError("reference vector has zero mean magnitude")
+        return (row[0] / n) / (row[1] / n)
+
+    rows = [DiffRow(T - k, rel(s[k]), rel(s[T + k]), s[k][2] / n, s[T + k][2] / n)
+            for k in range(T)]
+    return rows, rel(s[2 * T])

@@ -235,6 +235,30 @@ class NcclSampler:
             self.graph = g
         self.graph.replay()
 
+    def sample(self, seed: int, graph: bool = False):
+        """Run one denoise and return rank 0's Trajectory (None on other ranks)."""
+        self.run(seed, graph=graph)
+        return self.result().trajectory
+
+    def traffic_census(self) -> dict:
+        """This rank's ε-exchange bytes per round vs the closed form.
+
+        One all-gather per cycle (len(cycles) rounds); per round a rank sends
+        N*s bytes and receives (d-1)*N*s (the all-gather replaces the
+        reference's NOISE + SAMPLE_BCAST pair, whose ledger is 2(d-1)*M per
+        full cycle, protocol/ledger.py:120-123).
+        """
+        o = self.ops
+        es = 8 if o.code == _lib.PS_F64 else 4
+        per = o.n * es
+        lines = ["round,cycle_len,sent_bytes,received_bytes"]
+        for i, cyc in enumerate(self.cycles):
+            lines.append(f"{i},{len(cyc)},{per},{(self.world - 1) * per}")
+        rounds = len(self.cycles)
+        return {"rounds": o.gathers, "sent": rounds * per,
+                "received": rounds * (self.world - 1) * per,
+                "ok": o.gathers == rounds, "csv": "\n".join(lines) + "\n"}
+
     def result(self) -> RunResult:
         import torch
 

@@ -72,11 +72,11 @@ static float attn_run(const float* qkv, float* out, int B, int L, int H, int D, 
   const int64_t nq = (int64_t)B * L * 3 * D, no = (int64_t)B * L * D;
   const int64_t nqp = (int64_t)B * L * 3 * H * (DH ? DH : 1);
   __nv_bfloat16 *qb = nullptr, *ob = nullptr;
-  float* qf = nullptr;
+  float *qf = nullptr, *out_f32 = nullptr;
   int rc = 0;
   float us = -1.f;
   if (cudaMalloc(&qb, std::max(nq, nqp) * 2) || cudaMalloc(&ob, no * 2) ||
-      cudaMalloc(&qf, nq * 4)) {
+      cudaMalloc(&qf, nq * 4) || cudaMalloc(&out_f32, no * 4)) {
     rc = fail(PS_ECUDA, "attn_run: cudaMalloc");
   }
   if (!rc) {
@@ -105,9 +105,12 @@ static float attn_run(const float* qkv, float* out, int B, int L, int H, int D, 
     aa.dh = dh;
     aa.scale = 1.0f / sqrtf((float)dh);
     aa.out_bf16 = ob;
+    if (impl == 5) aa.qkv = qkv ? qkv : qf;  // fp32 path reads the unrounded fp32 qkv
+    if (impl == 5) aa.out_bf16 = nullptr, aa.out_f32 = out_f32;
     auto go = [&]() -> int {
       if (impl == 2) return fmha_launch(map, fa, st);
-      if (!launch_attn_tc(AM_BF16, aa, B, st)) return fail(PS_EUNSUP, "head_dim unsupported");
+      if (!launch_attn_tc(impl == 5 ? AM_TF32X3 : AM_BF16, aa, B, st))
+        return fail(PS_EUNSUP, "head_dim unsupported");
       return check_launch("attn_tc");
     };
     if (!rc) rc = go();
@@ -125,13 +128,17 @@ static float attn_run(const float* qkv, float* out, int B, int L, int H, int D, 
       cudaEventDestroy(a);
       cudaEventDestroy(b);
     }
-    if (!rc && out) bf16_to_f32_n<<<(unsigned)((no + 255) / 256), 256, 0, st>>>(ob, out, no);
+    if (!rc && out && impl == 5)
+      cudaMemcpyAsync(out, out_f32, no * 4, cudaMemcpyDeviceToDevice, st);
+    else if (!rc && out)
+      bf16_to_f32_n<<<(unsigned)((no + 255) / 256), 256, 0, st>>>(ob, out, no);
     cudaError_t se = cudaStreamSynchronize(st);
     if (!rc && se != cudaSuccess) rc = fail((int)se, std::string("attn: ") + cudaGetErrorString(se));
   }
   cudaFree(qb);
   cudaFree(ob);
   cudaFree(qf);
+  cudaFree(out_f32);
   *rc_out = rc;
   return us;
 }
@@ -144,19 +151,21 @@ extern "C" {
 
 int ps_attn_test(const float* qkv, float* out, int B, int L, int H, int D, int impl, void* cs) {
   PS_CHECK_ARG(qkv && out && B >= 1 && L >= 1 && H >= 1 && D % H == 0, "bad attention arguments");
-  PS_CHECK_ARG(impl >= 1 && impl <= 4, "impl: 1 mma.sync, 2 tcgen05 (auto), 3/4 tcgen05 1/2 tiles");
+  PS_CHECK_ARG(impl >= 1 && impl <= 5,
+               "impl: 1 mma.sync bf16, 2 tcgen05 (auto), 3/4 tcgen05 1/2 tiles, 5 mma.sync 3xTF32");
   int rc = 0;
   g_fmha_nq = impl == 3 ? 1 : (impl == 4 ? 2 : 0);
-  attn_run(qkv, out, B, L, H, D, impl >= 2 ? 2 : 1, 0, as_stream(cs), &rc);
+  attn_run(qkv, out, B, L, H, D, impl == 5 ? 5 : (impl >= 2 ? 2 : 1), 0, as_stream(cs), &rc);
   g_fmha_nq = 0;
   return rc;
 }
 
 float ps_attn_probe(int B, int L, int H, int D, int impl, int iters) {
-  if (B < 1 || L < 1 || H < 1 || D % H || iters < 1 || impl < 1 || impl > 4) return -1.f;
+  if (B < 1 || L < 1 || H < 1 || D % H || iters < 1 || impl < 1 || impl > 5) return -1.f;
   int rc = 0;
   g_fmha_nq = impl == 3 ? 1 : (impl == 4 ? 2 : 0);
-  float us = attn_run(nullptr, nullptr, B, L, H, D, impl >= 2 ? 2 : 1, iters, 0, &rc);
+  float us = attn_run(nullptr, nullptr, B, L, H, D, impl == 5 ? 5 : (impl >= 2 ? 2 : 1), iters, 0,
+                      &rc);
   g_fmha_nq = 0;
   return rc ? -1.f : us;
 }

@@ -18,6 +18,8 @@
 // written in the proj GEMM's operand format.
 #pragma once
 
+#include <cstdlib>
+
 #include "dit_kernels.cuh"
 
 namespace ps {
@@ -289,12 +291,16 @@ __global__ void __launch_bounds__(NW * 32) attn_tc_kernel(const __grid_constant_
 // order (deterministic). 4x more warps in flight than one warp per query
 // tile, which is what a latency-bound L = 256 attention needs.
 constexpr int KS_KB = 32;
+constexpr int KS_KW_DEFAULT = 8;  // measured: 8 warps x one 32-key block beat 4 x two at L=256
 
 template <int DHP>
 struct KsCfg {
   static constexpr int ST = DHP + 4;
   static constexpr int WSTAGE = 2 * KS_KB * ST;  // K + V floats per stage per warp
-  static size_t smem(int kw) { return (size_t)kw * 2 * WSTAGE * sizeof(float); }
+  // stages per warp: 2 (double-buffered loop over key blocks), or 1 when the
+  // 8-warp variant covers the whole sequence with one block per warp
+  static constexpr int nst(int kw) { return kw == 8 ? 1 : 2; }
+  static size_t smem(int kw) { return (size_t)kw * nst(kw) * WSTAGE * sizeof(float); }
 };
 
 template <int MODE, int DHP, int KW>
@@ -313,7 +319,8 @@ __global__ void __launch_bounds__(KW * 32) attn_ks_kernel(const __grid_constant_
   const int q0 = blockIdx.x * FA_QW;
   const int nkb = (L + KS_KB - 1) / KS_KB;
   const int dh4 = dh >> 2;
-  float* wbuf = ks_smem + (size_t)warp * 2 * C::WSTAGE;
+  constexpr int NST = C::nst(KW);
+  float* wbuf = ks_smem + (size_t)warp * NST * C::WSTAGE;
 
   if (DHP > dh)  // zero the pad columns of this warp's stages once
     for (int r = lane; r < 2 * 2 * KS_KB; r += 32)
@@ -363,13 +370,13 @@ __global__ void __launch_bounds__(KW * 32) attn_ks_kernel(const __grid_constant_
   int it = 0;
   for (int kb = warp; kb < nkb; kb += KW, ++it) {
     if (kb + KW < nkb) {
-      stage_load(kb + KW, (it + 1) & 1);
+      stage_load(kb + KW, (it + 1) % NST);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     __syncwarp();
-    const float* Ks = wbuf + (it & 1) * C::WSTAGE;
+    const float* Ks = wbuf + (it % NST) * C::WSTAGE;
     const float* Vs = Ks + KS_KB * ST;
     const int k0 = kb * KS_KB;
     float s[KS_KB / 8][4];
@@ -522,19 +529,34 @@ __global__ void __launch_bounds__(KW * 32) attn_ks_kernel(const __grid_constant_
   }
 }
 
-constexpr int KS_KW = 4;
+// warps per CTA of the key-split kernel (keys split KW ways). Tuned on B200
+// (profiles/r1b_attn_probe.txt); PS_ATTN_KS_WARPS=4|8 overrides for probes.
+static inline int ks_warps() {
+  static int kw = [] {
+    const char* e = getenv("PS_ATTN_KS_WARPS");
+    return (e && atoi(e) == 8) ? 8 : (e && atoi(e) == 4 ? 4 : KS_KW_DEFAULT);
+  }();
+  return kw;
+}
 
-template <int MODE, int DHP>
-static inline void launch_ks(const AttnArgs& a, int B, cudaStream_t st) {
-  const size_t smem = KsCfg<DHP>::smem(KS_KW);
+template <int MODE, int DHP, int KW>
+static inline void launch_ks_w(const AttnArgs& a, int B, cudaStream_t st) {
+  const size_t smem = KsCfg<DHP>::smem(KW);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_ks_kernel<MODE, DHP, KS_KW>,
+    cudaFuncSetAttribute(attn_ks_kernel<MODE, DHP, KW>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   dim3 grid((a.L + FA_QW - 1) / FA_QW, a.H, B);
-  launch_pdl(attn_ks_kernel<MODE, DHP, KS_KW>, grid, dim3(KS_KW * 32), smem, st, a);
+  launch_pdl(attn_ks_kernel<MODE, DHP, KW>, grid, dim3(KW * 32), smem, st, a);
+}
+
+template <int MODE, int DHP>
+static inline void launch_ks(const AttnArgs& a, int B, cudaStream_t st) {
+  // the 8-warp variant is single-buffered: one 32-key block per warp
+  if (ks_warps() == 8 && a.L <= 8 * KS_KB) launch_ks_w<MODE, DHP, 8>(a, B, st);
+  else launch_ks_w<MODE, DHP, 4>(a, B, st);
 }
 
 constexpr int FA_NW = 2;  // 32 queries per CTA: more CTAs for short sequences

@@ -301,6 +301,9 @@ def config_block(args, cfg, world):
 USE_NCCL = False  # set in main(): world > 1, or --force-nccl (1-rank NCCL path check)
 
 
+EXCHANGE = {"want": "peer", "used": None}  # --exchange; what the NCCL-group runs used
+
+
 def make_sampler(w, sched, rcfg, world, record=False, external_init=False):
     if world == 1 and not (USE_NCCL and rcfg.strategy == "parastep"):
         from paper_2505_14741_b200.engines import DeviceSampler
@@ -308,6 +311,15 @@ def make_sampler(w, sched, rcfg, world, record=False, external_init=False):
         return DeviceSampler(w, sched, rcfg, record=record, external_init=external_init)
     from paper_2505_14741_b200.protocol import NcclSampler
 
+    if EXCHANGE["want"] == "peer":
+        try:
+            s = NcclSampler(w, sched, rcfg, record=record, external_init=external_init,
+                            exchange="peer")
+            EXCHANGE["used"] = "peer"
+            return s
+        except Exception as exc:  # IPC / P2P unavailable: the NCCL all-gather path
+            log(f"peer exchange unavailable ({exc}); using the NCCL all-gather")
+    EXCHANGE["used"] = "nccl"
     return NcclSampler(w, sched, rcfg, record=record, external_init=external_init)
 
 
@@ -523,6 +535,11 @@ def our_arm(args, cfg, world, rank, local):
         "samples_ms": ms,
     }
     out.update(extra)
+    if USE_NCCL:
+        out["config"]["exchange"] = {
+            "peer": "peer memory: CUDA-IPC-mapped lane eps read over NVLink by the fused "
+                    "apply kernel, release/acquire flags (csrc/peer.cu)",
+            "nccl": "NCCL all_gather_into_tensor"}.get(EXCHANGE["used"], EXCHANGE["used"])
     print(json.dumps(out), flush=True)
 
 
@@ -537,6 +554,9 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=3,
                     help="reference arm: sampler steps timed per bench step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", choices=("peer", "nccl"), default="peer",
+                    help="multi-GPU eps exchange: CUDA-IPC peer memory read by the fused apply "
+                         "kernel (default), or the NCCL all-gather")
     ap.add_argument("--force-nccl", action="store_true",
                     help="run the NCCL rank loop even at one rank (path check under torchrun)")
     args = ap.parse_args()
@@ -549,6 +569,7 @@ def main():
         return
     global USE_NCCL
     USE_NCCL = world > 1 or args.force_nccl
+    EXCHANGE["want"] = args.exchange
     if USE_NCCL:
         import torch
         import torch.distributed as dist

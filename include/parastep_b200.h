@@ -213,6 +213,27 @@ int ps_unet_forward(ps_unet* h, const float* x, const int32_t* host_ts, int B, f
 int ps_unet_destroy(ps_unet* h);
 int ps_unet_kernels_per_forward(const ps_unet* h);
 
+/* ---- peer-memory eps exchange (multi-GPU ParaStep, one process per GPU) ---
+ * Replaces the per-round all-gather: ranks export their double-buffered
+ * lane-eps buffers and ready flags through CUDA IPC (64-byte handles), a
+ * publisher stores base+round+1 into every rank's ready[me] with
+ * system-scope release (ps_peer_signal; `slots` = device array of the world
+ * flag addresses), a consumer waits on its local ready[0..count) with
+ * acquire (ps_peer_wait), and ps_sched_cycle then reads the peers' eps over
+ * NVLink directly. ps_peer_epoch_advance moves `base` on by 2^20 per run. */
+int ps_dev_alloc(size_t bytes, void** out_dev_ptr); /* zeroed cudaMalloc (IPC-exportable) */
+int ps_dev_free(void* dev_ptr);
+int ps_ipc_get_handle(void* dev_ptr, void* out_handle64);
+int ps_ipc_open_handle(const void* handle64, void** out_dev_ptr);
+int ps_ipc_close(void* dev_ptr);
+int ps_peer_signal(uint64_t* const* slots, int world, const uint64_t* base, uint64_t round,
+                   void* cuda_stream);
+int ps_peer_wait(const uint64_t* ready, int count, const uint64_t* base, uint64_t round,
+                 void* cuda_stream);
+int ps_peer_epoch_advance(uint64_t* base, void* cuda_stream);
+/* async device-to-device (or peer) copy on the stream */
+int ps_copy(void* dst, const void* src, size_t bytes, void* cuda_stream);
+
 /* ---- trajectory files and diagnostics on device --------
  * ps_traj_pack writes the reference's binary trajectory file
  * (trajectory_io.py:100-110, "PSTJ" v1, little-endian float64 payload) into

@@ -97,6 +97,15 @@ _SIGS = {
                                   C.c_void_p, C.c_void_p]),
     "ps_unet_destroy": (C.c_int, [C.c_void_p]),
     "ps_unet_kernels_per_forward": (C.c_int, [C.c_void_p]),
+    "ps_dev_alloc": (C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
+    "ps_dev_free": (C.c_int, [C.c_void_p]),
+    "ps_ipc_get_handle": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "ps_ipc_open_handle": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "ps_ipc_close": (C.c_int, [C.c_void_p]),
+    "ps_peer_signal": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64, C.c_void_p]),
+    "ps_peer_wait": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64, C.c_void_p]),
+    "ps_peer_epoch_advance": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "ps_copy": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "ps_traj_pack_bytes": (C.c_int64, [C.c_int, C.c_int64]),
     "ps_traj_pack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                C.c_void_p, C.c_int, C.c_int64, C.c_int, C.c_void_p, C.c_void_p]),

@@ -67,7 +67,7 @@ def rank_loop(ops, T: int, warmup: int, p: int, rank: int, cycles: list[list[int
             e_local = ops.forward(x if rank == 0 else lane_x, cyc[rank], "lane")
         else:
             e_local = ops.zeros("lane")
-        gathered = ops.allgather(e_local)
+        gathered = ops.allgather(e_local, c)
         ops.record(T - cyc[0], gathered[:c])
         if mine:
             cache = ops.keep_cache(gathered[rank])
@@ -77,11 +77,107 @@ def rank_loop(ops, T: int, warmup: int, p: int, rank: int, cycles: list[list[int
     return x
 
 
+class _OwnedDev:
+    """Exposes memory from ps_dev_alloc (our cudaMalloc, this process's device)
+    to torch through the CUDA array interface."""
+
+    def __init__(self, ptr: int, shape: tuple, typestr: str):
+        self.__cuda_array_interface__ = {"shape": shape, "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+class _PeerVec:
+    """A rank's eps vector in (possibly a peer's IPC-mapped) device memory:
+    only its address is used - by ps_sched_cycle and the record copy - so no
+    torch tensor ever spans devices."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.ptr, self.nbytes = int(ptr), nbytes
+
+    def data_ptr(self) -> int:
+        return self.ptr
+
+
+class PeerExchange:
+    """Peer-memory eps exchange over CUDA IPC (csrc/peer.cu), one per rank.
+
+    Local memory exported to every peer: ``e_buf[2][n]`` (this rank's lane
+    eps, double-buffered by round parity) and ``ready[world]`` (flag j holds
+    base + round + 1 once rank j's eps of that round is written). The
+    bootstrap (handle exchange) runs over the given process group, which may
+    be gloo: no data moves through it.
+    """
+
+    def __init__(self, n: int, dtype, rank: int, world: int, group=None):
+        import ctypes as C
+
+        import torch
+        import torch.distributed as dist
+
+        self.lib = _lib.load(require_gpu=True)
+        self.n, self.rank, self.world = n, rank, world
+        es = torch.empty(0, dtype=dtype).element_size()
+        # own cudaMalloc allocations: an IPC handle maps the allocation base
+        self.owned = []
+        for nbytes in (2 * n * es, 8 * world):
+            ptr = C.c_void_p()
+            _lib.check(self.lib.ps_dev_alloc(nbytes, C.byref(ptr)), "exchange alloc")
+            self.owned.append(ptr.value)
+        self.e_buf = torch.as_tensor(_OwnedDev(self.owned[0], (2, n), "<f8" if es == 8 else "<f4"),
+                                     device="cuda")
+        self.ready = torch.as_tensor(_OwnedDev(self.owned[1], (world,), "<i8"), device="cuda")
+        self.base = torch.zeros(1, dtype=torch.int64, device="cuda")
+        torch.cuda.synchronize()
+        hs = []
+        for ptr in self.owned:
+            h = (C.c_char * 64)()
+            _lib.check(self.lib.ps_ipc_get_handle(ptr, h), "ipc handle")
+            hs.append(bytes(h))
+        allh = [None] * world
+        dist.all_gather_object(allh, hs, group=group)
+        self.opened = []
+        e_ptr, r_ptr = [], []
+        for p in range(world):
+            if p == rank:
+                e_ptr.append(_lib.ptr(self.e_buf))
+                r_ptr.append(_lib.ptr(self.ready))
+                continue
+            ptrs = []
+            for hb in allh[p]:
+                out = C.c_void_p()
+                _lib.check(self.lib.ps_ipc_open_handle(hb, C.byref(out)), "ipc open")
+                ptrs.append(out.value)
+                self.opened.append(out.value)
+            e_ptr.append(ptrs[0])
+            r_ptr.append(ptrs[1])
+        # round parity -> every rank's eps vector of that parity
+        self.views = [[_PeerVec(e_ptr[p] + par * n * es, n * es) for p in range(world)]
+                      for par in (0, 1)]
+        # where this rank's "ready" goes on every rank: ready_p[rank]
+        self.slots = torch.tensor([r_ptr[p] + 8 * rank for p in range(world)], dtype=torch.int64,
+                                  device="cuda")
+        dist.barrier(group=group)
+
+    def close(self):
+        """Unmap the peers' buffers and free ours (after a barrier: peers may
+        still read this rank's memory until every rank is done)."""
+        for p in self.opened:
+            self.lib.ps_ipc_close(p)
+        self.opened = []
+        self.e_buf = self.ready = None
+        for p in self.owned:
+            self.lib.ps_dev_free(p)
+        self.owned = []
+
+
 class CudaRankOps:
-    """Device buffers + C-ABI launches + NCCL all-gather for one rank."""
+    """Device buffers + C-ABI launches + the per-round eps exchange for one rank:
+    ``exchange="nccl"`` (all_gather_into_tensor) or ``"peer"`` (PeerExchange:
+    IPC-mapped peer buffers read by the fused apply kernel over NVLink)."""
 
     def __init__(self, w, sched: NoiseSchedule, cfg: RunConfig, rank: int, world: int,
-                 group=None, record: bool = False, external_init: bool = False):
+                 group=None, record: bool = False, external_init: bool = False,
+                 exchange: str = "nccl"):
         import torch
 
         self.torch = torch
@@ -109,11 +205,21 @@ class CudaRankOps:
         self.persist_cache = any(len(b) > len(a) for a, b in zip(cyc, cyc[1:]))
         self.launches = 0
         self.gathers = 0
+        if exchange not in ("nccl", "peer"):
+            raise ConfigError(f"unknown exchange {exchange!r}")
+        self.exchange = exchange
+        self.px = PeerExchange(n, tdt, rank, world, group) if exchange == "peer" else None
+        self.round = 0
 
     def _p(self, t) -> int:
         return _lib.ptr(t)
 
     def init(self):
+        self.round = 0
+        if self.px is not None:
+            _lib.check(self.lib.ps_peer_epoch_advance(self._p(self.px.base), _lib.stream_ptr()),
+                       "peer epoch")
+            self.launches += 1
         if not self.external_init:
             _lib.check(self.lib.ps_rng_normal_dev(
                 self._p(self.x), self.n, self._p(self.seed_buf), stream_id(PURPOSE_INIT, 0), 0,
@@ -123,6 +229,8 @@ class CudaRankOps:
 
     def forward(self, x, t, slot):
         out = self.e_warm if slot == "warm" else self.e_local
+        if slot != "warm" and self.px is not None:
+            out = self.px.e_buf[self.round % 2]  # written in place, read by peers
         self.w.forward_device(x.view(1, -1), [t], self.T, out.view(1, -1))
         self.launches += self.w.kernels_per_forward(1)
         return out
@@ -130,22 +238,47 @@ class CudaRankOps:
     def zeros(self, slot):
         return self.e_local  # idle rank: contents ignored by every receiver
 
-    def allgather(self, e):
+    def allgather(self, e, active: int | None = None):
+        if self.px is not None:
+            # publish this round's eps (already in e_buf[parity]) to every
+            # rank, wait for the `active` lanes' flags; the apply kernel then
+            # reads the peers' vectors in place over NVLink
+            active = self.world if active is None else active
+            k, st = self.round, _lib.stream_ptr()
+            if self.rank < active:
+                _lib.check(self.lib.ps_peer_signal(self._p(self.px.slots), self.world,
+                                                   self._p(self.px.base), k, st), "peer signal")
+            _lib.check(self.lib.ps_peer_wait(self._p(self.px.ready), active,
+                                             self._p(self.px.base), k, st), "peer wait")
+            self.launches += 2
+            self.gathers += 1
+            self.round += 1
+            return self.px.views[k % 2]
         import torch.distributed as dist
 
         dist.all_gather_into_tensor(self.gathered, e, group=self.group)
         self.gathers += 1
+        self.round += 1
         return [self.gathered[i] for i in range(self.world)]
 
     def keep_cache(self, e):
+        if isinstance(e, _PeerVec):  # own slot of the peer exchange: a local buffer
+            e = self.px.e_buf[(self.round - 1) % 2]
         if self.persist_cache:
             self.cache_buf.copy_(e)
             return self.cache_buf
         return e
 
     def record(self, k, eps_list):
-        if self.record_on:
-            self.rec_e[k:k + len(eps_list)].copy_(self.torch.stack(eps_list))
+        if not self.record_on:
+            return
+        if eps_list and isinstance(eps_list[0], _PeerVec):
+            row = self.n * self.rec_e.element_size()
+            for i, e in enumerate(eps_list):
+                _lib.check(self.lib.ps_copy(self._p(self.rec_e) + (k + i) * row, e.ptr, row,
+                                            _lib.stream_ptr()), "record copy")
+            return
+        self.rec_e[k:k + len(eps_list)].copy_(self.torch.stack(eps_list))
 
     def apply_roll(self, x, apply_ts, eps_list, roll_ts, cache):
         es = x.element_size()
@@ -191,7 +324,7 @@ class NcclSampler:
     """
 
     def __init__(self, w, sched: NoiseSchedule, cfg: RunConfig, group=None, record=False,
-                 external_init=False):
+                 external_init=False, exchange: str = "nccl"):
         import torch.distributed as dist
 
         _check(w, sched, cfg, STRATEGY_PARASTEP)
@@ -203,7 +336,8 @@ class NcclSampler:
             raise ConfigError(f"degree {cfg.degree} != world size {self.world}")
         self.cfg = cfg
         self.cycles = plan_cycles(cfg)
-        self.ops = CudaRankOps(w, sched, cfg, self.rank, self.world, group, record, external_init)
+        self.ops = CudaRankOps(w, sched, cfg, self.rank, self.world, group, record, external_init,
+                               exchange)
         self.graph = None
 
     def _launch(self):

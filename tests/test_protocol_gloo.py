@@ -38,7 +38,7 @@ class OracleOps:
     def zeros(self, slot):
         return np.zeros(self.n)
 
-    def allgather(self, e):
+    def allgather(self, e, active=None):
         out = [torch.zeros(self.n, dtype=torch.float64) for _ in range(self.world)]
         dist.all_gather(out, torch.from_numpy(np.ascontiguousarray(e)))
         self.gathers += 1

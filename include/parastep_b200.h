@@ -141,6 +141,14 @@ int ps_dit_create(const ps_dit_config* cfg, const ps_dit_weights* w, ps_dit** ou
 int ps_dit_forward(ps_dit* h, const float* x, const int32_t* host_ts, int B, float* eps_out,
                    void* cuda_stream);
 int ps_dit_destroy(ps_dit* h);
+/* Per-run conditioning table (rows t = 0..T of every adaLN vector, 16 steps
+ * per GEMV launch): reserve allocates (call outside graph capture), condition
+ * fills it on the stream (capturable; the samplers run it at the start of
+ * every denoise), clear returns forwards to per-forward conditioning. Rows
+ * are bit-identical to the per-forward path. */
+int ps_dit_condition_reserve(ps_dit* h, int T);
+int ps_dit_condition(ps_dit* h, int T, void* cuda_stream);
+int ps_dit_condition_clear(ps_dit* h);
 /* algorithmic FLOPs of one forward of one sample (GEMMs + attention) */
 double ps_dit_flops(const ps_dit* h);
 

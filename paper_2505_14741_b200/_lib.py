@@ -84,6 +84,9 @@ _SIGS = {
     "ps_dit_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int32), C.c_int,
                                  C.c_void_p, C.c_void_p]),
     "ps_dit_destroy": (C.c_int, [C.c_void_p]),
+    "ps_dit_condition_reserve": (C.c_int, [C.c_void_p, C.c_int]),
+    "ps_dit_condition": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    "ps_dit_condition_clear": (C.c_int, [C.c_void_p]),
     "ps_dit_flops": (C.c_double, [C.c_void_p]),
     "ps_dit_kernels_per_forward": (C.c_int, [C.c_void_p]),
     "ps_dit_bench_gemm": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]),

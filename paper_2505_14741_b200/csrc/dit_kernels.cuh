@@ -203,6 +203,8 @@ struct LnModArgs {
   int rows, D, L;
   const float* mod;  // per lane base of modulation vector block
   int64_t mod_stride;
+  int use_rows;              // lane b reads mod row mod_row[b] (else row b)
+  int32_t mod_row[GV_MAXB];
   int shift_off, scale_off;
   float* out_f32;
   __nv_bfloat16* out_bf16;
@@ -275,8 +277,9 @@ static __global__ void __launch_bounds__(256) ln_mod_kernel(const __grid_constan
   for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
   const float rstd = rsqrtf(q / p.D + 1e-6f);
   const int b = row / p.L;
-  const float4* sh = reinterpret_cast<const float4*>(p.mod + (int64_t)b * p.mod_stride + p.shift_off);
-  const float4* sc = reinterpret_cast<const float4*>(p.mod + (int64_t)b * p.mod_stride + p.scale_off);
+  const int64_t mrow = p.use_rows ? p.mod_row[b] : b;
+  const float4* sh = reinterpret_cast<const float4*>(p.mod + mrow * p.mod_stride + p.shift_off);
+  const float4* sc = reinterpret_cast<const float4*>(p.mod + mrow * p.mod_stride + p.scale_off);
 #pragma unroll
   for (int u = 0; u < LN_MAXV; ++u) {
     const int i = lane + 32 * u;

@@ -34,17 +34,26 @@ struct Epi {
   int act;  // 1 = GELU-tanh
   // EPI_NCHW: eps[b * n_latent + n * hw + p] = acc + bias, m = b * hw + p
   int hw;
+  // per-lane rows of gate / vec: lane b reads row lane_row[b] (a per-run
+  // conditioning table indexed by t) when use_rows, else row b
+  int use_rows;
+  int32_t lane_row[16];
   // EPI_STORE bf16 into a head-padded operand: column n = (w*H + h)*pad_dh + d
   // goes to (w*H + h)*pad_DH + d of a row of N/pad_dh*pad_DH (0 = dense)
   int pad_dh, pad_DH;
 };
+
+__device__ __forceinline__ int64_t lane_row(const Epi& e, int m) {
+  const int b = m / e.L;
+  return e.use_rows ? e.lane_row[b] : b;
+}
 
 __device__ __forceinline__ int64_t padded_index(const Epi& e, int m, int n, int N) {
   return (int64_t)m * (N / e.pad_dh * e.pad_DH) + (n / e.pad_dh) * e.pad_DH + n % e.pad_dh;
 }
 
 __device__ __forceinline__ float epi_add_val(const Epi& e, int m, int n, int64_t idx, float v) {
-  if (e.vec) v += e.vec[(int64_t)(m / e.L) * e.vec_stride + n];
+  if (e.vec) v += e.vec[lane_row(e, m) * e.vec_stride + n];
   if (e.resid) v += e.resid[idx];
   return e.act ? gelu_tanh_f(v) : v;
 }
@@ -69,8 +78,7 @@ __device__ __forceinline__ void epi_store(const Epi& e, int m, int n, int N, flo
       break;
     }
     case EPI_RESID: {
-      const int b = m / e.L;
-      e.resid[idx] = fmaf(e.gate[(int64_t)b * e.gate_stride + n], v, e.resid[idx]);
+      e.resid[idx] = fmaf(e.gate[lane_row(e, m) * e.gate_stride + n], v, e.resid[idx]);
       break;
     }
     case EPI_UNPATCH: {
@@ -164,7 +172,7 @@ __device__ __forceinline__ void epi_store16(const Epi& e, int m, int n, int N, c
     }
   } else if (e.mode == EPI_ADD) {
     if (e.vec) {
-      const float* vv = e.vec + (int64_t)(m / e.L) * e.vec_stride + n;
+      const float* vv = e.vec + lane_row(e, m) * e.vec_stride + n;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const float4 a = *reinterpret_cast<const float4*>(vv + 4 * q);
@@ -197,7 +205,7 @@ __device__ __forceinline__ void epi_store16(const Epi& e, int m, int n, int N, c
       *reinterpret_cast<uint4*>(e.out_bf16 + base + 8) = make_uint4(u[4], u[5], u[6], u[7]);
     }
   } else {  // EPI_RESID
-    const float* g = e.gate + (int64_t)(m / e.L) * e.gate_stride + n;
+    const float* g = e.gate + lane_row(e, m) * e.gate_stride + n;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       float4 r = *reinterpret_cast<const float4*>(e.resid + base + 4 * q);
@@ -251,7 +259,7 @@ __device__ __forceinline__ void epi_store4(const Epi& e, int m, int n, int N, co
     }
   } else if (e.mode == EPI_ADD) {
     if (e.vec) {
-      const float4 a = *reinterpret_cast<const float4*>(e.vec + (int64_t)(m / e.L) * e.vec_stride + n);
+      const float4 a = *reinterpret_cast<const float4*>(e.vec + lane_row(e, m) * e.vec_stride + n);
       x[0] += a.x; x[1] += a.y; x[2] += a.z; x[3] += a.w;
     }
     if (e.resid) {
@@ -264,7 +272,7 @@ __device__ __forceinline__ void epi_store4(const Epi& e, int m, int n, int N, co
     if (e.out) st_f32(e.out);
     if (e.out_bf16) st_bf16(e.out_bf16);
   } else {  // EPI_RESID
-    const float4 g = *reinterpret_cast<const float4*>(e.gate + (int64_t)(m / e.L) * e.gate_stride + n);
+    const float4 g = *reinterpret_cast<const float4*>(e.gate + lane_row(e, m) * e.gate_stride + n);
     float4 r = *reinterpret_cast<const float4*>(e.resid + base);
     r.x = fmaf(g.x, x[0], r.x);
     r.y = fmaf(g.y, x[1], r.y);

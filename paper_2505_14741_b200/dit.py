@@ -143,6 +143,17 @@ class DiTWeights:
         D, M = s.hidden, B * s.tokens
         return [(M, 3 * D, D), (M, D, D), (M, s.mlp_hidden, D), (M, D, s.mlp_hidden)][which]
 
+    def reserve_conditioning(self, T: int) -> None:
+        """Allocate the per-run conditioning table for steps 0..T (not capturable)."""
+        _lib.check(self._lib.ps_dit_condition_reserve(self._h, T), "condition reserve")
+
+    def prepare_conditioning(self, T: int, stream=None) -> None:
+        """Fill rows 0..T of the conditioning table on the stream (capturable)."""
+        _lib.check(self._lib.ps_dit_condition(self._h, T, _lib.stream_ptr(stream)), "condition")
+
+    def clear_conditioning(self) -> None:
+        _lib.check(self._lib.ps_dit_condition_clear(self._h), "condition clear")
+
     def forward_device(self, x, ts, T: int, out, stream=None) -> None:
         """x, out: CUDA float32 [B, data_dim]; ts: B step indices (<= 1000). Async."""
         B = len(ts)

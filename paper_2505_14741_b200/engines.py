@@ -214,7 +214,8 @@ class DeviceSampler:
     """
 
     def __init__(self, w, sched: NoiseSchedule, cfg: RunConfig, record: bool = True,
-                 batched: bool | None = None, external_init: bool = False):
+                 batched: bool | None = None, external_init: bool = False,
+                 condition_table: bool = True):
         import torch
 
         _check(w, sched, cfg, None)
@@ -249,6 +250,11 @@ class DeviceSampler:
         self.external_init = external_init
         self.launches = 0  # kernels issued by one run (counted at issue time)
         self._steps = {t: step_coeffs(sched, t) for t in range(1, self.T + 1)}
+        # batched per-run conditioning (DiT): the table is filled at the start
+        # of every run; off = each forward conditions itself (same bits)
+        self.condition_table = condition_table and hasattr(w, "prepare_conditioning")
+        if self.condition_table:
+            w.reserve_conditioning(self.T)
 
     # ------------------------------------------------------------ launches
     def _k(self, t: int) -> int:
@@ -299,6 +305,11 @@ class DeviceSampler:
         self.launches = 0
         self._init_x()
         T = self.T
+        if self.condition_table:
+            # the t-only conditioning of every step of this run, batched
+            # (16 steps per launch) instead of recomputed inside each forward
+            self.w.prepare_conditioning(T)
+            self.launches += 3 * (-(-(T + 1) // 16))
         if cfg.strategy == STRATEGY_SEQUENTIAL:
             for t in range(T, 0, -1):
                 k = self._k(t)

@@ -205,6 +205,8 @@ class CudaRankOps:
         self.persist_cache = any(len(b) > len(a) for a, b in zip(cyc, cyc[1:]))
         self.launches = 0
         self.gathers = 0
+        if hasattr(w, "reserve_conditioning"):
+            w.reserve_conditioning(self.T)
         if exchange not in ("nccl", "peer"):
             raise ConfigError(f"unknown exchange {exchange!r}")
         self.exchange = exchange
@@ -216,6 +218,9 @@ class CudaRankOps:
 
     def init(self):
         self.round = 0
+        if hasattr(self.w, "prepare_conditioning"):  # batched t-only conditioning of the run
+            self.w.prepare_conditioning(self.T)
+            self.launches += 3 * (-(-(self.T + 1) // 16))
         if self.px is not None:
             _lib.check(self.lib.ps_peer_epoch_advance(self._p(self.px.base), _lib.stream_ptr()),
                        "peer epoch")

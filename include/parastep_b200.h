@@ -149,6 +149,7 @@ int ps_dit_destroy(ps_dit* h);
 int ps_dit_condition_reserve(ps_dit* h, int T);
 int ps_dit_condition(ps_dit* h, int T, void* cuda_stream);
 int ps_dit_condition_clear(ps_dit* h);
+int ps_dit_condition_chunk(const ps_dit* h); /* steps per conditioning launch (x3 GEMVs) */
 /* algorithmic FLOPs of one forward of one sample (GEMMs + attention) */
 double ps_dit_flops(const ps_dit* h);
 

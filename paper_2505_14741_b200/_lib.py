@@ -87,6 +87,7 @@ _SIGS = {
     "ps_dit_condition_reserve": (C.c_int, [C.c_void_p, C.c_int]),
     "ps_dit_condition": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "ps_dit_condition_clear": (C.c_int, [C.c_void_p]),
+    "ps_dit_condition_chunk": (C.c_int, [C.c_void_p]),
     "ps_dit_flops": (C.c_double, [C.c_void_p]),
     "ps_dit_kernels_per_forward": (C.c_int, [C.c_void_p]),
     "ps_dit_bench_gemm": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]),

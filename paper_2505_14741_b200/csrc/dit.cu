@@ -304,13 +304,25 @@ int ps_dit_condition_reserve(ps_dit* h, int T) {
   return 0;
 }
 
+// steps per conditioning launch: as many GEMV rows as fit the 200 KB smem the
+// GEMV stages its inputs in (16, or 12 for a 1920-wide bf16 adaLN)
+int ps_dit_condition_chunk(const ps_dit* h) {
+  if (!h) return 0;
+  const int D = h->D;
+  const bool abf = h->Wada_bf16 != nullptr;
+  const size_t row_bytes = std::max(abf ? gemv_smem<__nv_bfloat16>(1, D) : gemv_smem<float>(1, D),
+                                    gemv_smem<float>(1, std::max(D, h->freq_dim)));
+  return std::max(1, std::min(GV_MAXB, (int)((200u << 10) / row_bytes)));
+}
+
 int ps_dit_condition(ps_dit* h, int T, void* cs) {
   PS_CHECK_ARG(h && T >= 1 && T + 1 <= h->cond_cap, "conditioning table not reserved for T");
   cudaStream_t st = as_stream(cs);
   const int D = h->D;
   const bool abf = h->Wada_bf16 != nullptr;
-  for (int t0 = 0; t0 <= T; t0 += GV_MAXB) {
-    const int nb = std::min(GV_MAXB, T + 1 - t0);
+  const int chunk = ps_dit_condition_chunk(h);
+  for (int t0 = 0; t0 <= T; t0 += chunk) {
+    const int nb = std::min(chunk, T + 1 - t0);
     int32_t ts[GV_MAXB];
     for (int i = 0; i < nb; ++i) ts[i] = t0 + i;
     int rc;

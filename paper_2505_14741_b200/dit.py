@@ -147,9 +147,12 @@ class DiTWeights:
         """Allocate the per-run conditioning table for steps 0..T (not capturable)."""
         _lib.check(self._lib.ps_dit_condition_reserve(self._h, T), "condition reserve")
 
-    def prepare_conditioning(self, T: int, stream=None) -> None:
-        """Fill rows 0..T of the conditioning table on the stream (capturable)."""
+    def prepare_conditioning(self, T: int, stream=None) -> int:
+        """Fill rows 0..T of the conditioning table on the stream (capturable);
+        returns the kernel launches issued."""
         _lib.check(self._lib.ps_dit_condition(self._h, T, _lib.stream_ptr(stream)), "condition")
+        chunk = int(self._lib.ps_dit_condition_chunk(self._h))
+        return 3 * (-(-(T + 1) // chunk))
 
     def clear_conditioning(self) -> None:
         _lib.check(self._lib.ps_dit_condition_clear(self._h), "condition clear")

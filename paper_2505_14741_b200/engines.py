@@ -308,8 +308,7 @@ class DeviceSampler:
         if self.condition_table:
             # the t-only conditioning of every step of this run, batched
             # (16 steps per launch) instead of recomputed inside each forward
-            self.w.prepare_conditioning(T)
-            self.launches += 3 * (-(-(T + 1) // 16))
+            self.launches += self.w.prepare_conditioning(T)
         if cfg.strategy == STRATEGY_SEQUENTIAL:
             for t in range(T, 0, -1):
                 k = self._k(t)

@@ -219,8 +219,7 @@ class CudaRankOps:
     def init(self):
         self.round = 0
         if hasattr(self.w, "prepare_conditioning"):  # batched t-only conditioning of the run
-            self.w.prepare_conditioning(self.T)
-            self.launches += 3 * (-(-(self.T + 1) // 16))
+            self.launches += self.w.prepare_conditioning(self.T)
         if self.px is not None:
             _lib.check(self.lib.ps_peer_epoch_advance(self._p(self.px.base), _lib.stream_ptr()),
                        "peer epoch")

@@ -64,8 +64,8 @@ __global__ void transpose_convert_kernel(const float* __restrict__ W, int K, int
 }
 
 int tc_operand_maps(TcOperand& op, int precision) {
-  for (int i = 0; i < 3; ++i) {
-    const int box = TC_BM >> i;  // multicast slice of 128 / CN rows
+  for (int i = 0; i < 1; ++i) {
+    const int box = TC_BM;
     if (precision == 1) {
       if (int rc = tc_make_map(&op.map_main[i], op.bf16, 2, op.cols, op.rows, box)) return rc;
     } else {
@@ -106,9 +106,7 @@ static int g_dbg = 0;  // ps_gemm_probe only
 static int g_split_enable = 1;  // probe bit 5 disables split-K
 static int g_force_in_cta = 0;  // probe bit 6 runs the segments in-CTA (no cluster)
 static int g_sc_max = 8;        // test hook: cap on cluster CTAs along K (forces the hybrid)
-// A multicast across N-tile CTAs: measured slower than independent loads at
-// every DiT/U-Net shape on B200 (profiles/), so off unless a probe asks for it
-static int g_cn_max = 1;        // probe: bit 9 = up to 4 CTAs share A, bit 8 = up to 2
+
 
 static int bn_index(int bn) { return bn == 32 ? 0 : (bn == 64 ? 1 : 2); }
 
@@ -118,8 +116,10 @@ static int launch(const TcLayer& L, const TcOperand& A, int M, int N, int K, con
   using C = TcCfg<KIND, BN>;
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(gemm_tc_kernel<KIND, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         C::SMEM);
+    cudaFuncSetAttribute(gemm_tc_kernel<KIND, BN, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(gemm_tc_kernel<KIND, BN, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   });
   const int tiles_n = (N + BN - 1) / BN, tiles_m = (M + TC_BM - 1) / TC_BM;
   // segments as a cluster only while the whole grid is co-resident (clusters
@@ -138,15 +138,13 @@ static int launch(const TcLayer& L, const TcOperand& A, int M, int N, int K, con
       }
     }
   }
-  // A multicast: CN adjacent N-tile CTAs share each A tile (one 128/CN-row
-  // slice loaded per CTA, broadcast to the group); cluster (CN, 1, sc) <= 8
-  int cn = 1;
-  while (cn * 2 <= g_cn_max && cn * 2 * sc <= 8 && tiles_n >= cn * 2) cn *= 2;
   if ((L.splits / sc) * BN > 512)
     return fail(PS_EUNSUP, "gemm_tc: segment accumulators exceed the 512 TMEM columns");
-  const TcSplit sk{L.splits, sc, cn};
+  TcSplit sk{L.splits, sc, {}};
+  const int nk_all = (K + C::BK - 1) / C::BK;
+  for (int g = 0; g <= L.splits; ++g) sk.seg[g] = (int)((int64_t)g * nk_all / L.splits);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((tiles_n + cn - 1) / cn * cn, tiles_m, sk.cluster);
+  cfg.gridDim = dim3(tiles_n, tiles_m, sk.cluster);
   cfg.blockDim = dim3(TC_THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
@@ -154,19 +152,19 @@ static int launch(const TcLayer& L, const TcOperand& A, int M, int N, int K, con
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   at[1].id = cudaLaunchAttributeClusterDimension;
-  at[1].val.clusterDim.x = cn;
+  at[1].val.clusterDim.x = 1;
   at[1].val.clusterDim.y = 1;
   at[1].val.clusterDim.z = sk.cluster;
   cfg.attrs = at;
-  cfg.numAttrs = (sk.cluster > 1 || cn > 1) ? 2 : 1;
-  const int bi = bn_index(BN), ai = cn == 1 ? 0 : (cn == 2 ? 1 : 2);
-  cudaError_t err;
-  if (KIND == KIND_BF16)
-    err = cudaLaunchKernelEx(&cfg, gemm_tc_kernel<KIND, BN>, A.map_main[ai], A.map_main[ai],
-                             L.map_b[bi], L.map_b[bi], M, N, K, e, g_dbg, sk);
-  else
-    err = cudaLaunchKernelEx(&cfg, gemm_tc_kernel<KIND, BN>, A.map_main[ai], A.map_lo[ai],
-                             L.map_b[bi], L.map_blo[bi], M, N, K, e, g_dbg, sk);
+  cfg.numAttrs = sk.cluster > 1 ? 2 : 1;
+  const int bi = bn_index(BN);
+  const CUtensorMap& alo = KIND == KIND_BF16 ? A.map_main[0] : A.map_lo[0];
+  const CUtensorMap& blo = KIND == KIND_BF16 ? L.map_b[bi] : L.map_blo[bi];
+  cudaError_t err = g_dbg ? cudaLaunchKernelEx(&cfg, gemm_tc_kernel<KIND, BN, true>, A.map_main[0],
+                                               alo, L.map_b[bi], blo, M, N, K, e, g_dbg, sk)
+                          : cudaLaunchKernelEx(&cfg, gemm_tc_kernel<KIND, BN, false>,
+                                               A.map_main[0], alo, L.map_b[bi], blo, M, N, K, e, 0,
+                                               sk);
   if (err != cudaSuccess) return fail((int)err, std::string("gemm_tc: ") + cudaGetErrorString(err));
   return check_launch("gemm_tc");
 }
@@ -397,7 +395,6 @@ int ps_gemm_test(const float* A, const float* W, const float* bias, float* Cout,
 float ps_gemm_probe(int M, int N, int K, int precision, int dbg, int iters) {
   g_split_enable = (dbg & 32) ? 0 : 1;  // bit 5: disable split-K
   g_force_in_cta = (dbg & 64) ? 1 : 0;  // bit 6: segments in-CTA
-  g_cn_max = (dbg & 512) ? 4 : ((dbg & 256) ? 2 : 1);
   dbg &= 31;
   float *A = nullptr, *W = nullptr, *C = nullptr;
   if (cudaMalloc(&A, (size_t)M * K * 4) || cudaMalloc(&W, (size_t)K * N * 4) ||
@@ -437,7 +434,6 @@ float ps_gemm_probe(int M, int N, int K, int precision, int dbg, int iters) {
   cudaFree(C);
   g_split_enable = 1;
   g_force_in_cta = 0;
-  g_cn_max = 1;
   return us;
 }
 

@@ -33,8 +33,9 @@ struct TcOperand {
   float* hi = nullptr;
   float* lo = nullptr;
   int rows = 0, cols = 0;
-  // A maps per multicast width CN = 1, 2, 4 (boxes of 128/CN rows): index
-  // log2(CN). [0] of map_main is the full 128-row box. bf16 or hi / tf32-lo.
+  // A maps (128-row boxes): bf16 or tf32-hi / tf32-lo. (Entries 1-2 held
+  // 64/32-row boxes for an A-tile TMA multicast across N-tile CTAs, which
+  // measured slower at every DiT/U-Net shape and was removed.)
   CUtensorMap map_main[3];
   CUtensorMap map_lo[3];
 };
@@ -100,17 +101,6 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
-// multicast: the box lands at the same smem offset in every CTA of cta_mask
-// and signals each one's mbarrier at the same offset
-__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                               int x, int y, uint16_t cta_mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "h"(cta_mask)
-      : "memory");
-}
-
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -159,23 +149,6 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                : "memory");
 }
 
-// arrive on the same-offset mbarrier of every CTA in cta_mask once the
-// previously issued MMAs complete
-__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t cta_mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-      " [%0], %1;" ::"r"(smem_u32(bar)),
-      "h"(cta_mask)
-      : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
-  uint32_t remote;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(cta));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
-               : "memory");
-}
-
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   uint32_t r[16];
   asm volatile(
@@ -201,11 +174,12 @@ struct TcCfg {
   static constexpr int B_BYTES = BN * BK_BYTES;
   static constexpr int NOPS = KIND == KIND_BF16 ? 1 : 2;  // main (+lo) copies
   static constexpr int STAGE_BYTES = NOPS * (A_BYTES + B_BYTES);
-  // as many stages as the budget holds (3..6; tf3x BN=128 takes 3 x 64 KB).
-  // Measured: deeper rings (up to 10) do not speed up the small-M mainloop,
-  // which is bound by per-SM TMA ingest (~70 GB/s/SM), not latency x depth
+  // 4 stages (3 for tf3x BN=128: 3 x 64 KB). Measured: deeper rings (up to
+  // 10) do not speed up the small-M mainloop, which is bound by per-SM TMA
+  // ingest (~70 GB/s/SM), and 6 stages cost the large-M GEMMs ~25%
+  // (CogVideoX fc1 753 -> 959 us, same box A/B)
   static constexpr int STAGES_FIT = TC_SMEM_BUDGET / STAGE_BYTES;
-  static constexpr int STAGES = STAGES_FIT < 3 ? 3 : (STAGES_FIT > 6 ? 6 : STAGES_FIT);
+  static constexpr int STAGES = STAGES_FIT < 3 ? 3 : (STAGES_FIT > 4 ? 4 : STAGES_FIT);
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
 };
@@ -225,9 +199,9 @@ struct TcCfg {
 struct TcSplit {
   int splits;   // S: K segments (fixed per layer)
   int cluster;  // SC: CTAs along K per tile (1 = all segments in one CTA; S/SC each)
-  int cn;       // N-tile CTAs per cluster sharing one multicast A tile (1, 2, 4)
+  int seg[9];   // K-block bounds of the segments: segment g = [seg[g], seg[g+1])
 };
-// cluster dims (cn, 1, cluster): rank = x + cn * z
+// cluster dims (1, 1, cluster): rank = z
 
 // DSMEM load of a peer's partial tile. Not volatile / no memory clobber: the
 // data is immutable between the two cluster barriers that bracket the
@@ -248,15 +222,17 @@ __device__ __forceinline__ void cluster_sync_all() {
                    : "memory");
 }
 
-// diagnostics: dbg bit 4 records clock64() phase stamps of CTA (0,0,0) here
+// diagnostics (DIAG instantiation only): dbg bit 4 records clock64() phase
+// stamps of CTA (0,0,0) here. Production launches use DIAG = false, so no
+// diagnostic branch or clock read sits in the producer / MMA loops.
 __device__ long long g_tc_ts[16];
-#define TC_STAMP(i)                                                     \
-  do {                                                                  \
-    if ((dbg & 16) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) \
-      g_tc_ts[i] = clock64();                                           \
+#define TC_STAMP(i)                                                          \
+  do {                                                                       \
+    if (DIAG && (dbg & 16) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) \
+      g_tc_ts[i] = clock64();                                                \
   } while (0)
 
-template <int KIND, int BN>
+template <int KIND, int BN, bool DIAG>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapAlo,
                    const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapBlo,
@@ -274,17 +250,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * BN;
-  const int CN = sk.cn, cx = blockIdx.x % CN;
-  // A multicast group: the CN N-tile CTAs of this K segment
-  const uint16_t grp = (uint16_t)(((1u << CN) - 1u) << (CN * (sk.cluster > 1 ? blockIdx.z : 0)));
+  if (!DIAG) dbg = 0;
   const int nk_all = (K + C::BK - 1) / C::BK;
   const int S = sk.splits;
   const int SC = sk.cluster;            // CTAs sharing the K range (1 = all in this CTA)
   const int G = S / SC;                 // consecutive segments per CTA
   const bool in_cta = SC == 1;
   const int zc = in_cta ? 0 : (int)blockIdx.z;
-  auto seg_lo = [&](int sg) { return (int)((int64_t)sg * nk_all / S); };
-  const int kb0 = seg_lo(zc * G), kb1 = seg_lo((zc + 1) * G);
+  const int kb0 = sk.seg[zc * G], kb1 = sk.seg[(zc + 1) * G];
   const int nk = kb1 - kb0;
   // TMEM columns: one BN-wide accumulator per segment of this CTA (power of 2 >= 32)
   uint32_t tcols = 32;
@@ -301,7 +274,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int s = 0; s < TC_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CN);  // every CTA of the multicast group releases the stage
+      mbar_init(&empty[s], 1);
     }
     mbar_init(accum, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -316,7 +289,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  if (CN > 1) cluster_sync_all();  // peers' barriers initialised before any multicast
   if (threadIdx.x == 0) TC_STAMP(1);
   // the prologue above overlaps the predecessor's tail (PDL); operands and
   // epilogue inputs are only touched after it completes
@@ -336,30 +308,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_expect_tx(&full[s], C::STAGE_BYTES);
       if (kb == 0) TC_STAMP(3);
       const int kx = (kb0 + kb) * C::BK;
-      if (CN == 1) {
-        tma_load_2d(st, &mapA, &full[s], kx, m0);
-        if (KIND == KIND_TF32X3) tma_load_2d(st + C::A_BYTES + C::B_BYTES, &mapAlo, &full[s], kx, m0);
-      } else {
-        // this CTA's 128/CN-row slice of the shared A tile, to the whole group
-        const int rs = TC_BM / CN, ro = cx * rs;
-        tma_load_2d_mc(st + ro * 128, &mapA, &full[s], kx, m0 + ro, grp);
-        if (KIND == KIND_TF32X3)
-          tma_load_2d_mc(st + C::A_BYTES + C::B_BYTES + ro * 128, &mapAlo, &full[s], kx, m0 + ro,
-                         grp);
-      }
+      tma_load_2d(st, &mapA, &full[s], kx, m0);
       tma_load_2d(st + C::A_BYTES, &mapB, &full[s], kx, n0);
-      if (KIND == KIND_TF32X3)
+      if (KIND == KIND_TF32X3) {
+        tma_load_2d(st + C::A_BYTES + C::B_BYTES, &mapAlo, &full[s], kx, m0);
         tma_load_2d(st + 2 * C::A_BYTES + C::B_BYTES, &mapBlo, &full[s], kx, n0);
+      }
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer
     constexpr uint32_t idesc = make_idesc(KIND, TC_BM, BN);
-    int seg = 0, seg_start = 0, seg_end = seg_lo(zc * G + 1) - kb0;
+    int seg = 0, seg_start = 0, seg_end = sk.seg[zc * G + 1] - kb0;
     for (int kb = 0; kb < nk; ++kb) {
       if (kb == seg_end) {  // next segment of this CTA: fresh accumulator columns
         ++seg;
         seg_start = kb;
-        seg_end = seg_lo(zc * G + seg + 1) - kb0;
+        seg_end = sk.seg[zc * G + seg + 1] - kb0;
       }
       const uint32_t dacc = tmem + (uint32_t)(seg * BN);
       const int s = kb % TC_STAGES;
@@ -371,8 +335,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const uint64_t a0 = smem_desc_sw128(st);
       const uint64_t b0 = smem_desc_sw128(st + C::A_BYTES);
       if (dbg & 1) {
-        for (int c = 0; c < CN; ++c)
-          mbar_arrive_remote(&empty[s], (uint32_t)(__ffs(grp) - 1 + c));
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
         continue;
       }
 #pragma unroll
@@ -388,8 +351,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           umma<KIND>(dacc, alo + koff, b0 + koff, idesc, 1u);
         }
       }
-      if (CN == 1) umma_commit(&empty[s]);
-      else umma_commit_mc(&empty[s], grp);
+      umma_commit(&empty[s]);
     }
     if (dbg & 1)
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(accum)) : "memory");
@@ -417,7 +379,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       if ((dbg & 4) == 0 && row < M && n0 + c < N) epi_store16(e, row, n0 + c, N, v);
     }
-    if (CN > 1) cluster_sync_all();  // peers' last multicast commits have landed on our barriers
   } else {
     // this CTA's G segment partials -> own smem (the stage ring is drained:
     // all MMAs completed, every multicast into it has landed)
@@ -455,8 +416,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
         for (int sg = 0; sg < 8; ++sg)
           if (sg < S)
-            a[u][sg] = G == 1 ? ld_dsmem_f4(src, (uint32_t)(cx + CN * sg))
-                              : ld_dsmem_f4(src + (sg % G) * PTILE, (uint32_t)(cx + CN * (sg / G)));
+            a[u][sg] = G == 1 ? ld_dsmem_f4(src, (uint32_t)sg)
+                              : ld_dsmem_f4(src + (sg % G) * PTILE, (uint32_t)(sg / G));
       }
 #pragma unroll
       for (int u = 0; u < 2; ++u) {

@@ -28,15 +28,24 @@ static __global__ void peer_signal_kernel(uint64_t* const* slots, int world, con
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(slots[p]), "l"(v) : "memory");
 }
 
+// A peer that never signals (crashed rank, broken P2P mapping) must not hang
+// the box: after ~20 s of spinning the wait traps, which surfaces as a CUDA
+// error on this rank instead of a silent deadlock.
+constexpr long long PEER_WAIT_LIMIT_CYCLES = 40000000000ll;
+
 static __global__ void peer_wait_kernel(const uint64_t* ready, int count, const uint64_t* base,
                                         uint64_t round) {
   const uint64_t v = *base + round + 1ull;
   if (threadIdx.x < count) {
+    const long long t0 = clock64();
     uint64_t got;
     do {
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(got) : "l"(ready + threadIdx.x)
                    : "memory");
-      if (got < v) __nanosleep(64);
+      if (got < v) {
+        __nanosleep(64);
+        if (clock64() - t0 > PEER_WAIT_LIMIT_CYCLES) __trap();
+      }
     } while (got < v);
   }
   __syncthreads();

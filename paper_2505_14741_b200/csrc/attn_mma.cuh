@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(KW * 32) attn_ks_kernel(const __grid_constant_
   float* wbuf = ks_smem + (size_t)warp * NST * C::WSTAGE;
 
   if (DHP > dh)  // zero the pad columns of this warp's stages once
-    for (int r = lane; r < 2 * 2 * KS_KB; r += 32)
+    for (int r = lane; r < NST * 2 * KS_KB; r += 32)
       for (int d = dh; d < DHP; ++d) wbuf[r * ST + d] = 0.f;
   auto stage_load = [&](int kb, int stg) {
     float* Kd = wbuf + stg * C::WSTAGE;
@@ -584,8 +584,8 @@ static inline bool launch_attn_tc(int mode, const AttnArgs& a, int B, cudaStream
       case 32: ks ? launch_ks<AM_BF16, 32>(a, B, st) : launch_fa<AM_BF16, 32>(a, B, st); return true;
       case 64: ks ? launch_ks<AM_BF16, 64>(a, B, st) : launch_fa<AM_BF16, 64>(a, B, st); return true;
       case 80: ks ? launch_ks<AM_BF16, 80>(a, B, st) : launch_fa<AM_BF16, 80>(a, B, st); return true;
-      case 128:
-        ks ? launch_ks<AM_BF16, 128>(a, B, st) : launch_fa<AM_BF16, 128>(a, B, st);
+      case 128:  // the key-split stages would exceed 227 KB of smem at this width
+        launch_fa<AM_BF16, 128>(a, B, st);
         return true;
       default: return false;
     }

@@ -78,6 +78,17 @@ def test_attention_peaked_scores_rescale():
         _check(_attn(qkv, B, L, H, D, impl), _ref(qkv, B, L, H, D))
 
 
+@pytest.mark.parametrize("dh", [32, 72, 128])
+def test_attention_mma_padded_head_dims(dh):
+    """The mma.sync key-split kernel (8 single-buffered warps at L <= 256)
+    with zero-padded head dims (72 -> 80)."""
+    B, L, H = 1, 256, 3
+    D = dh * H
+    g = torch.Generator(device="cuda").manual_seed(dh)
+    qkv = torch.randn((B * L, 3 * D), device="cuda", generator=g)
+    _check(_attn(qkv, B, L, H, D, 1), _ref(qkv, B, L, H, D))
+
+
 def test_attention_long_cogvideox_head():
     """One CogVideoX-shaped head: 17,550 tokens (137 full key blocks + 14)."""
     B, L, H = 1, 17550, 1

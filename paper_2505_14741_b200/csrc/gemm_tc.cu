@@ -169,6 +169,46 @@ static int launch(const TcLayer& L, const TcOperand& A, int M, int N, int K, con
   return check_launch("gemm_tc");
 }
 
+// 2-SM (cta_group::2) launch: 256 x 256 tiles on CTA pairs, bf16, no split.
+static int g_force_2sm = -1;  // test hook: -1 auto, 0 never, 1 always (when legal)
+
+static int launch2(const TcLayer& L, const TcOperand& A, int M, int N, int K, const Epi& e,
+                   cudaStream_t st) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(gemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TC2_SMEM);
+  });
+  const int tiles_m = (M + TC_BM - 1) / TC_BM;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((tiles_m + 1) / 2 * 2, (N + TC2_BN - 1) / TC2_BN, 1);
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = TC2_SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = 2;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  cudaError_t err =
+      cudaLaunchKernelEx(&cfg, gemm_tc2_kernel, A.map_main[0], L.map_b[2], M, N, K, e);
+  if (err != cudaSuccess) return fail((int)err, std::string("gemm_tc2: ") + cudaGetErrorString(err));
+  return check_launch("gemm_tc2");
+}
+
+// A layer takes the 2-SM kernel when one lane alone fills several waves of
+// 128 x 128 tiles (decided from ref_rows, so every batch of the layer runs
+// the same kernel: a row's bits never depend on the batch).
+static bool use_2sm(const TcLayer& L, int precision) {
+  if (precision != 1 || L.splits != 1 || g_force_2sm == 0) return false;
+  if (g_force_2sm == 1) return true;
+  const int tiles = ((L.ref_rows + TC_BM - 1) / TC_BM) * ((L.N + 127) / 128);
+  return L.ref_rows >= 2048 && tiles >= 2 * 148;
+}
+
 // Tile plan. At small M the mainloop is bound by per-SM TMA ingest
 // (~70 GB/s/SM measured, profiles/): a CTA loads K/S x (128 + BN) operand
 // elements, so wide N tiles (less re-reading of the shared A tile) plus
@@ -303,6 +343,7 @@ int tc_prepare(TcWeights& w, TcActs& acts, const std::vector<const float*>& Ws,
 int tc_gemm(const TcWeights& w, int layer, const TcOperand& A, int M, int N, int K, const Epi& e,
             int precision, cudaStream_t st) {
   const TcLayer& L = w.layers[layer];
+  if (use_2sm(L, precision)) return launch2(L, A, M, N, K, e, st);
   const int bn = choose_bn(L, precision, M, N);
   if (precision == 1) {
     if (bn == 32) return launch<KIND_BF16, 32>(L, A, M, N, K, e, st);
@@ -355,10 +396,12 @@ int ps_gemm_test(const float* A, const float* W, const float* bias, float* Cout,
   cudaStream_t st = as_stream(cs);
   // impl 3: tensor cores with the K segments forced in-CTA (cluster-free);
   // must equal impl 2 bit-for-bit (test_gemm_split_paths_bitwise)
-  // impl 4: at most 2 cluster CTAs along K (each running S/2 segments)
+  // impl 4: at most 2 cluster CTAs along K (each running S/2 segments);
+  // impl 5 / 6: bf16 2-SM (cta_group::2) kernel forced on / off
   g_force_in_cta = impl == 3 ? 1 : 0;
   g_sc_max = impl == 4 ? 2 : 8;
-  if (impl == 3 || impl == 4) impl = 2;
+  g_force_2sm = impl == 5 ? 1 : (impl == 6 ? 0 : -1);
+  if (impl >= 3) impl = 2;
   Epi e{};
   e.mode = EPI_STORE;
   e.bias = bias;
@@ -385,6 +428,7 @@ int ps_gemm_test(const float* A, const float* W, const float* bias, float* Cout,
   tc_release(w, acts);
   g_force_in_cta = 0;
   g_sc_max = 8;
+  g_force_2sm = -1;
   return rc;
 }
 

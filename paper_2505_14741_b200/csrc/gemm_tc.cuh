@@ -446,6 +446,144 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (threadIdx.x == 0) TC_STAMP(8);
 }
 
+// ------------------------------------------------------------------ 2-SM GEMM
+// Large-M bf16 GEMM on CTA pairs (tcgen05 cta_group::2): one MMA instruction
+// computes a 256 x 256 tile, A rows split across the pair (each CTA loads
+// its own 128 rows) and B (the [N][K] weight copy) split likewise (each
+// CTA loads 128 of the 256 N rows), so per CTA the operand traffic per
+// output is half that of the 128 x 128 single-CTA tile - the large-M GEMMs
+// are bound by L2 -> SM operand delivery, not by the tensor pipe.
+//   both CTAs:  TMA of their A / B halves, signalling the LEADER's full
+//               barrier (rank 0; the peer bit of the smem address cleared)
+//   leader:     waits full, issues tcgen05.mma.cta_group::2 (M=256, N=256),
+//               commits to BOTH CTAs' empty barriers (multicast), finally to
+//               both CTAs' accumulator barriers
+//   both CTAs:  epilogue from their own TMEM (128 rows x 256 columns)
+// No split-K (S = 1): a row's accumulation order is the same K order as the
+// single-CTA kernel.
+constexpr int TC2_BN = 256, TC2_STAGES = 4;
+constexpr int TC2_A_BYTES = 128 * 128, TC2_B_BYTES = 128 * 128;  // per CTA, per 64-K slab
+constexpr int TC2_STAGE_BYTES = TC2_A_BYTES + TC2_B_BYTES;
+constexpr int TC2_SMEM = TC2_STAGES * TC2_STAGE_BYTES + 1024 + 256;
+
+static __global__ void __launch_bounds__(TC_THREADS, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                    int M, int N, int K, const __grid_constant__ Epi e) {
+  extern __shared__ __align__(1024) uint8_t tc2_smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(tc2_smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TC2_STAGES * TC2_STAGE_BYTES);
+  uint64_t* empty = full + TC2_STAGES;
+  uint64_t* accum = empty + TC2_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int m0 = blockIdx.x * TC_BM;             // consecutive M tiles form the pair
+  const int nb0 = blockIdx.y * TC2_BN;           // the pair's 256 N columns
+  const int nh0 = nb0 + (int)rank * 128;         // this CTA's half of B
+  const int nk = (K + 63) / 64;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&mapA);
+    tma_prefetch_desc(&mapB);
+    for (int s = 0; s < TC2_STAGES; ++s) {
+      mbar_init(&full[s], 1);   // leader only: its producer's arrive + both CTAs' bytes
+      mbar_init(&empty[s], 1);  // one multicast commit from the leader's MMA
+    }
+    mbar_init(accum, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TC2_BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  cluster_sync_all();  // the leader's barriers exist before the peer's TMA signals them
+  pdl_wait_and_release();
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer (both CTAs), completion on the leader's barrier
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % TC2_STAGES;
+      mbar_wait(&empty[s], ((kb / TC2_STAGES) & 1) ^ 1);
+      const uint32_t bar = smem_u32(&full[s]) & 0xFEFFFFFFu;  // rank-0 CTA's barrier
+      if (rank == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])),
+                     "r"(2 * TC2_STAGE_BYTES)
+                     : "memory");
+      uint8_t* st = smem + s * TC2_STAGE_BYTES;
+      const int kx = kb * 64;
+      asm volatile(
+          "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(st)),
+          "l"(reinterpret_cast<uint64_t>(&mapA)), "r"(bar), "r"(kx), "r"(m0)
+          : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(st + TC2_A_BYTES)),
+          "l"(reinterpret_cast<uint64_t>(&mapB)), "r"(bar), "r"(kx), "r"(nh0)
+          : "memory");
+    }
+  } else if (warp == 1 && lane == 0 && rank == 0) {
+    // ---------------- MMA issuer (leader): M = 256 over the pair, N = 256
+    constexpr uint32_t idesc = make_idesc(KIND_BF16, 256, TC2_BN);
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % TC2_STAGES;
+      mbar_wait(&full[s], (kb / TC2_STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint8_t* st = smem + s * TC2_STAGE_BYTES;
+      const uint64_t a0 = smem_desc_sw128(st);
+      const uint64_t b0 = smem_desc_sw128(st + TC2_A_BYTES);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint64_t koff = (uint64_t)(k * 32) >> 4;
+        const uint32_t acc = (kb | k) ? 1u : 0u;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+            "l"(a0 + koff), "l"(b0 + koff), "r"(idesc), "r"(acc));
+      }
+      asm volatile(
+          "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+          " [%0], %1;" ::"r"(smem_u32(&empty[s])),
+          "h"((uint16_t)3)
+          : "memory");
+    }
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(smem_u32(accum)),
+        "h"((uint16_t)3)
+        : "memory");
+  }
+  __syncwarp();
+
+  // ---------------- epilogue: this CTA's 128 rows x 256 columns from its TMEM
+  mbar_wait(accum, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int row = m0 + warp * 32 + lane;
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll 1
+  for (int c = 0; c < TC2_BN; c += 16) {
+    float v[16];
+    tmem_ld16(trow + c, v);
+    if (row < M && nb0 + c < N) epi_store16(e, row, nb0 + c, N, v);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  cluster_sync_all();  // the peer's TMA / our commits are all done before either CTA exits
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TC2_BN));
+  }
+}
+
 // ------------------------------------------------------------------ host side
 int tc_prepare(TcWeights& w, TcActs& acts, const std::vector<const float*>& Ws,
                const std::vector<int>& Ks, const std::vector<int>& Ns, int max_rows, int ref_rows,

@@ -172,3 +172,22 @@ def test_gemm_split_paths_bitwise(shape, precision):
     c_hybrid = _gemm(A, W, bias, precision, 4)  # 2 cluster CTAs x S/2 segments each
     assert torch.equal(c_cluster, c_in_cta)
     assert torch.equal(c_cluster, c_hybrid)
+
+
+@pytest.mark.parametrize("shape", [(2048, 1024, 512), (2304, 1920, 1152), (4096, 640, 256),
+                                   (1920, 768, 128)])
+def test_gemm_2sm_vs_fp64_and_1sm(shape):
+    """bf16 GEMM on CTA pairs (tcgen05 cta_group::2, 256 x 256 tiles) vs fp64
+    and vs the single-CTA kernel (same K order per element)."""
+    M, N, K = shape
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = torch.randn((M, K), device="cuda", generator=g)
+    W = torch.randn((K, N), device="cuda", generator=g) / K ** 0.5
+    bias = torch.randn(N, device="cuda", generator=g)
+    c2 = _gemm(A, W, bias, 1, 5)
+    c1 = _gemm(A, W, bias, 1, 6)
+    ref = A.double() @ W.double() + bias.double()
+    scale = A.double().abs() @ W.double().abs() + bias.double().abs()
+    assert ((c2.double() - ref).abs() / scale).max().item() < 1e-2
+    print("2sm vs 1sm max abs diff", (c2 - c1).abs().max().item())
+    assert (c2 - c1).abs().max().item() <= 1e-3 * c1.abs().max().item()

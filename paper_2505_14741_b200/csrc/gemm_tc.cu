@@ -439,6 +439,8 @@ int ps_gemm_test(const float* A, const float* W, const float* bias, float* Cout,
 float ps_gemm_probe(int M, int N, int K, int precision, int dbg, int iters) {
   g_split_enable = (dbg & 32) ? 0 : 1;  // bit 5: disable split-K
   g_force_in_cta = (dbg & 64) ? 1 : 0;  // bit 6: segments in-CTA
+  const bool resid_epi = (dbg & 1024) != 0;  // bit 10: gated-residual epilogue (EPI_RESID)
+  g_force_2sm = (dbg & 2048) ? 0 : -1;       // bit 11: never the 2-SM kernel
   dbg &= 31;
   float *A = nullptr, *W = nullptr, *C = nullptr;
   if (cudaMalloc(&A, (size_t)M * K * 4) || cudaMalloc(&W, (size_t)K * N * 4) ||
@@ -455,6 +457,16 @@ float ps_gemm_probe(int M, int N, int K, int precision, int dbg, int iters) {
     Epi e{};
     e.mode = EPI_STORE;
     e.out = C;
+    float* ones = nullptr;
+    if (resid_epi) {
+      cudaMalloc(&ones, (size_t)N * 4);
+      cudaMemset(ones, 0, (size_t)N * 4);
+      e.mode = EPI_RESID;
+      e.resid = C;
+      e.gate = ones;
+      e.gate_stride = 0;
+      e.L = M;
+    }
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
@@ -470,6 +482,7 @@ float ps_gemm_probe(int M, int N, int K, int precision, int dbg, int iters) {
     us = ms * 1000.f / iters;
     cudaEventDestroy(a);
     cudaEventDestroy(b);
+    if (ones) cudaFree(ones);
   }
   cudaDeviceSynchronize();
   tc_release(w, acts);
@@ -478,6 +491,7 @@ float ps_gemm_probe(int M, int N, int K, int precision, int dbg, int iters) {
   cudaFree(C);
   g_split_enable = 1;
   g_force_in_cta = 0;
+  g_force_2sm = -1;
   return us;
 }
 

@@ -267,6 +267,10 @@ int ps_attn_test(const float* qkv, float* out, int B, int L, int H, int D, int i
                  void* cuda_stream);
 /* Diagnostic: mean device time (us) of `iters` back-to-back attention launches. */
 float ps_attn_probe(int B, int L, int H, int D, int impl, int iters);
+/* Tuning hook for the tcgen05 attention kernel: how many of every 4 exp2
+ * pairs run on the FMA-pipe polynomial instead of MUFU (-1 = built-in
+ * default per head width). Results stay deterministic for a fixed value. */
+int ps_fmha_set_poly(int pairs);
 
 #ifdef __cplusplus
 }

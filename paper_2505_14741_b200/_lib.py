@@ -118,6 +118,7 @@ _SIGS = {
     "ps_attn_test": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
                                C.c_int, C.c_void_p]),
     "ps_attn_probe": (C.c_float, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
+    "ps_fmha_set_poly": (C.c_int, [C.c_int]),
     "ps_gemm_test": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
                                C.c_int, C.c_int, C.c_int, C.c_void_p]),
 }

@@ -14,19 +14,32 @@ int fmha_make_map(CUtensorMap* m, const __nv_bfloat16* qkv_bf16, int rows, int c
   return tc_make_map(m, qkv_bf16, 2, cols, rows, FM_BK);
 }
 
-template <int DH, int NQ>
-static cudaError_t fmha_go(const CUtensorMap& map, const FmhaArgs& a, cudaStream_t st) {
+template <int DH, int NQ, int POLY>
+static cudaError_t fmha_go1(const CUtensorMap& map, const FmhaArgs& a, cudaStream_t st) {
   using C = FmCfg<DH, NQ>;
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(fmha_tc_kernel<DH, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         C::SMEM);
+    cudaFuncSetAttribute(fmha_tc_kernel<DH, NQ, POLY>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   });
-  return launch_pdl(fmha_tc_kernel<DH, NQ>, dim3((a.L + NQ * FM_BQ - 1) / (NQ * FM_BQ), a.H, a.B),
-                    dim3(C::THREADS), C::SMEM, st, map, a);
+  return launch_pdl(fmha_tc_kernel<DH, NQ, POLY>,
+                    dim3((a.L + NQ * FM_BQ - 1) / (NQ * FM_BQ), a.H, a.B), dim3(C::THREADS),
+                    C::SMEM, st, map, a);
 }
 
-static int g_fmha_nq = 0;  // test hook: force 1 or 2 query tiles per CTA (0 = auto)
+static int g_fmha_nq = 0;     // test hook: force 1 or 2 query tiles per CTA (0 = auto)
+static int g_fmha_poly = -1;  // test hook: exp pairs (of 4) on the polynomial (-1 = default)
+
+// default share of polynomial exps per configuration (measured, profiles/)
+template <int DH, int NQ>
+constexpr int fmha_poly_default() { return 0; }
+
+template <int DH, int NQ>
+static cudaError_t fmha_go(const CUtensorMap& map, const FmhaArgs& a, cudaStream_t st) {
+  const int poly = g_fmha_poly >= 0 ? g_fmha_poly : fmha_poly_default<DH, NQ>();
+  return poly == 0 ? fmha_go1<DH, NQ, 0>(map, a, st)
+                   : (poly == 1 ? fmha_go1<DH, NQ, 1>(map, a, st) : fmha_go1<DH, NQ, 2>(map, a, st));
+}
 
 int fmha_launch(const CUtensorMap& map, const FmhaArgs& a, cudaStream_t st) {
   const int DH = fmha_padded_dim(a.dh);
@@ -159,6 +172,18 @@ int ps_attn_test(const float* qkv, float* out, int B, int L, int H, int D, int i
   g_fmha_nq = 0;
   return rc;
 }
+
+int ps_fmha_set_poly(int pairs) {
+  PS_CHECK_ARG(pairs >= -1 && pairs <= 2, "pairs: -1 (default) or 0..2 of every 4");
+  g_fmha_poly = pairs;
+  return 0;
+}
+
+#ifdef FMHA_STAMPS
+int ps_fmha_stamps(long long* out) {  // diagnostic build only
+  return (int)cudaMemcpyFromSymbol(out, g_fm_ts, sizeof(g_fm_ts));
+}
+#endif
 
 float ps_attn_probe(int B, int L, int H, int D, int impl, int iters) {
   if (B < 1 || L < 1 || H < 1 || D % H || iters < 1 || impl < 1 || impl > 5) return -1.f;

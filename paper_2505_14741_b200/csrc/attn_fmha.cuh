@@ -28,6 +28,9 @@
 namespace ps {
 
 constexpr int FM_BQ = 128, FM_BK = 128;
+// TMEM columns: S buffers [0, 256), O [256, 256 + NQ*DH) (NQ*DH <= 128), and
+// the bf16 P buffers (64 columns each) at [384, 512)
+constexpr int FM_TP = 384;
 constexpr int FM_TILE = 128 * 128;  // bytes of one 128-row x 128-byte (64 bf16) box
 
 // DH = padded head width in smem/TMEM (64, or 128 for head_dim 72..128):
@@ -45,8 +48,7 @@ struct FmCfg {
   static constexpr int THREADS = (4 * NQ + 2) * 32;
   static constexpr int Q_OFF = 0;
   static constexpr int KV_OFF = NQ * NA * FM_TILE;  // stage s: K at +2s*NA*TILE, V at +(2s+1)*NA*TILE
-  static constexpr int P_OFF = KV_OFF + 2 * STAGES * NA * FM_TILE;  // 2 buffers x 2 key atoms
-  static constexpr int BAR_OFF = P_OFF + 4 * FM_TILE;
+  static constexpr int BAR_OFF = KV_OFF + 2 * STAGES * NA * FM_TILE;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
   static constexpr uint32_t TMEM_COLS = 512;
   static_assert(NQ == 1 || DH == 64, "two query tiles only for 64-wide heads (smem)");
@@ -93,13 +95,35 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
-template <int DH, int NQ>
+// exp2 on the FMA / ALU pipes: x = j + f with j = rint(x) (magic-number
+// round), 2^f by a degree-3 minimax polynomial on [-0.5, 0.5] (max relative
+// error 1.0e-4, far below P's bf16 rounding), 2^j added to the exponent
+// field. x is clamped at -127 so -inf (masked keys) gives exactly +0. Used
+// for a fixed share of the exps (POLY of every 4 pairs) to take load off the
+// MUFU unit (16 ex2 / clk / SM).
+__device__ __forceinline__ float poly_exp2(float x) {
+  x = fmaxf(x, -127.f);
+  const float r = x + 12582912.f;  // 1.5 * 2^23
+  const float f = x - (r - 12582912.f);
+  const float q = fmaf(fmaf(fmaf(0.0550089292f, f, 0.242210984f), f, 0.693282902f), f, 1.f);
+  return __int_as_float(__float_as_int(q) + (__float_as_int(r) << 23));
+}
+
+#ifdef FMHA_STAMPS
+__device__ long long g_fm_ts[9][32][4];
+#define FM_TS(role, j, k) \
+  do { if (blockIdx.x == 0 && blockIdx.y == 0 && (j) < 32) g_fm_ts[role][j][k] = clock64(); } while (0)
+#else
+#define FM_TS(role, j, k) do {} while (0)
+#endif
+
+template <int DH, int NQ, int POLY>
 __global__ void __launch_bounds__(FmCfg<DH, NQ>::THREADS, 1)
     fmha_tc_kernel(const __grid_constant__ CUtensorMap mapQKV, const __grid_constant__ FmhaArgs p) {
   using C = FmCfg<DH, NQ>;
   constexpr int W_TMA = 4 * NQ, W_MMA = 4 * NQ + 1;
   constexpr int NA = C::NA, FM_STAGES = C::STAGES, FM_Q_OFF = C::Q_OFF, FM_KV_OFF = C::KV_OFF,
-                FM_P_OFF = C::P_OFF, FM_BAR_OFF = C::BAR_OFF;
+                FM_BAR_OFF = C::BAR_OFF;
   constexpr uint32_t FM_TMEM_COLS = C::TMEM_COLS;
   extern __shared__ __align__(1024) uint8_t fm_smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -111,7 +135,8 @@ __global__ void __launch_bounds__(FmCfg<DH, NQ>::THREADS, 1)
   uint64_t* s_full = kv_empty + FM_STAGES;    // 2
   uint64_t* p_full = s_full + 2;              // 2
   uint64_t* pv_done = p_full + 2;             // 2
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
+  uint64_t* s_free = pv_done + 2;             // 2 (NQ = 2: S_t read out of TMEM)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_free + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q0 = blockIdx.x * FM_BQ * NQ, head = blockIdx.y, b = blockIdx.z;
@@ -130,6 +155,7 @@ __global__ void __launch_bounds__(FmCfg<DH, NQ>::THREADS, 1)
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 128);
       mbar_init(&pv_done[i], 1);
+      mbar_init(&s_free[i], 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -169,8 +195,9 @@ __global__ void __launch_bounds__(FmCfg<DH, NQ>::THREADS, 1)
       }
     }
   } else if (warp == W_MMA) {
-    if (lane == 0) {
-      // ---------------- MMA issuer
+    {
+      // ---------------- MMA issuer: the whole warp runs the loop (descriptors
+      // in uniform registers), one elected lane issues each tcgen05 op
       constexpr uint32_t idS = make_idesc(KIND_BF16, 128, 128);
       constexpr uint32_t idPV = make_idesc(KIND_BF16, 128, DH) | (1u << 16);  // B (V) MN-major
       // S_t(j) = Q_t K_j^T into S buffer `sb`
@@ -184,27 +211,24 @@ __global__ void __launch_bounds__(FmCfg<DH, NQ>::THREADS, 1)
         for (int k = 0; k < DH / 16; ++k) {  // atom k/4, +32 B along K inside it
           const uint64_t qd = smem_desc_sw128(qt + (k >> 2) * FM_TILE) + 2 * (k & 3);
           const uint64_t kd = smem_desc_sw128(kt + (k >> 2) * FM_TILE) + 2 * (k & 3);
-          umma<KIND_BF16>(tmem + 128 * sb, qd, kd, idS, k > 0 ? 1u : 0u);
+          umma_e<KIND_BF16>(tmem + 128 * sb, qd, kd, idS, k > 0 ? 1u : 0u);
         }
-        umma_commit(&s_full[sb]);
+        umma_commit_e(&s_full[sb]);
       };
       // O_t += P(buffer pb) V_j, once P has been written (p_full[pb], parity par)
       auto issue_pv = [&](int t, int j, int pb, int par) {
         mbar_wait(&p_full[pb], par);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const int s = j % FM_STAGES;
-        const uint8_t* pbuf = smem + FM_P_OFF + pb * 2 * FM_TILE;
+        const uint32_t tP = tmem + FM_TP + pb * 64;
         // V: MN-major, NA atoms of 64 dims at FM_TILE stride (LBO), 8-key groups at 1 KB (SBO)
         const uint64_t vd = (smem_desc_sw128(smem + FM_KV_OFF + (2 * s + 1) * NA * FM_TILE) &
                              ~(0x3FFFull << 16)) |
                             ((uint64_t)(FM_TILE >> 4) << 16);
         const uint32_t tO = tmem + 256 + (NQ == 1 ? 0 : t * DH);
 #pragma unroll
-        for (int k = 0; k < FM_BK / 16; ++k) {
-          // P: K-major, keys [64a, 64a+64) in atom column a; V: MN-major, 16 keys = 2048 B
-          const uint64_t pd = smem_desc_sw128(pbuf + (k >> 2) * FM_TILE) + 2 * (k & 3);
-          umma<KIND_BF16>(tO, pd, vd + (uint64_t)(k * 2048 >> 4), idPV, (j | k) ? 1u : 0u);
-        }
+        for (int k = 0; k < FM_BK / 16; ++k)  // P: 16 keys = 8 TMEM columns; V: 16 keys = 2048 B
+          umma_ts_e(tO, tP + 8 * k, vd + (uint64_t)(k * 2048 >> 4), idPV, (j | k) ? 1u : 0u);
       };
       mbar_wait(q_full, 0);
       if constexpr (NQ == 1) {
@@ -212,21 +236,34 @@ __global__ void __launch_bounds__(FmCfg<DH, NQ>::THREADS, 1)
         if (nkb > 1) issue_s(0, 1, 1);
         for (int j = 0; j < nkb; ++j) {
           issue_pv(0, j, j & 1, (j >> 1) & 1);
-          umma_commit(&kv_empty[j % FM_STAGES]);
-          umma_commit(&pv_done[j & 1]);
+          umma_commit_e(&kv_empty[j % FM_STAGES]);
+          umma_commit_e(&pv_done[j & 1]);
           if (j + 2 < nkb) issue_s(0, j + 2, j & 1);
         }
       } else {
+        // S_t(j+1) goes in as soon as the softmax has read S_t(j) out of TMEM
+        // (s_free, mid exp pass), ahead of P_t(j) V_j: the next block's
+        // scores are ready when the softmax finishes this one
         issue_s(0, 0, 0);
         issue_s(1, 0, 1);
         for (int j = 0; j < nkb; ++j) {
+          if (j + 1 < nkb) {
+            mbar_wait(&s_free[0], j & 1);
+            issue_s(0, j + 1, 0);
+          }
+          FM_TS(8, j, 0);
           issue_pv(0, j, 0, j & 1);
-          umma_commit(&pv_done[0]);
-          if (j + 1 < nkb) issue_s(0, j + 1, 0);  // tile 0's next scores under tile 1's softmax
+          umma_commit_e(&pv_done[0]);
+          FM_TS(8, j, 1);
+          if (j + 1 < nkb) {
+            mbar_wait(&s_free[1], j & 1);
+            issue_s(1, j + 1, 1);
+          }
+          FM_TS(8, j, 2);
           issue_pv(1, j, 1, j & 1);
-          umma_commit(&kv_empty[j % FM_STAGES]);
-          umma_commit(&pv_done[1]);
-          if (j + 1 < nkb) issue_s(1, j + 1, 1);
+          umma_commit_e(&kv_empty[j % FM_STAGES]);
+          umma_commit_e(&pv_done[1]);
+          FM_TS(8, j, 3);
         }
       }
     }
@@ -244,6 +281,7 @@ __global__ void __launch_bounds__(FmCfg<DH, NQ>::THREADS, 1)
     float m_ref = -INFINITY, l = 0.f;
     for (int j = 0; j < nkb; ++j) {
       mbar_wait(&s_full[buf(j)], par(j));
+      if (lane == 0) FM_TS(warp, j, 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       // Row max. NQ = 1: the whole 128-column S row is loaded once and kept in
       // registers for the exp pass; NQ = 2 (register-limited, 10 warps):
@@ -298,10 +336,12 @@ __global__ void __launch_bounds__(FmCfg<DH, NQ>::THREADS, 1)
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
       }
+      if (lane == 0) FM_TS(warp, j, 1);
       // the P buffer was last read by P V of block j-2 (NQ = 1) / j-1 (NQ = 2)
       if (NQ == 1 && j >= 2) mbar_wait(&pv_done[buf(j)], par(j - 2));
       if (NQ == 2 && j >= 1) mbar_wait(&pv_done[t], par(j - 1));
-      uint8_t* prow = smem + FM_P_OFF + buf(j) * 2 * FM_TILE + r * 128;
+      if (lane == 0) FM_TS(warp, j, 2);
+      const uint32_t prow = tmem + FM_TP + buf(j) * 64 + lane_off;  // bf16 pairs
       float ps[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int g = 0; g < FM_BK / CH; ++g) {  // exp2, row sum, bf16 P row
@@ -309,33 +349,39 @@ __global__ void __launch_bounds__(FmCfg<DH, NQ>::THREADS, 1)
 #pragma unroll
           for (int c = 0; c < CH / 32; ++c) tmem_ld32(srow + g * CH + c * 32, sv + c * 32);
           tmem_ld_wait();
+          if (g == FM_BK / CH - 1) {  // S_t fully read: the MMA warp may overwrite it
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_free[t]);
+          }
           if (valid < FM_BK) {
 #pragma unroll
             for (int i = 0; i < CH; ++i)
               if (g * CH + i >= valid) sv[i] = -INFINITY;
           }
         }
+        float pk[CH / 2];  // bf16 pairs of this group, column (key / 2)
 #pragma unroll
-        for (int h = 0; h < CH / 8; ++h) {  // 16-byte chunk of 8 keys
-          uint32_t u[4];
+        for (int h = 0; h < CH / 8; ++h) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const int i0 = h * 8 + 2 * q;  // masked keys hold -inf: exp2 -> +0
-            const float p0 = fast_exp2(fmaf(sv[i0], sl2, -m_ref));
-            const float p1 = fast_exp2(fmaf(sv[i0 + 1], sl2, -m_ref));
+            const float x0 = fmaf(sv[i0], sl2, -m_ref), x1 = fmaf(sv[i0 + 1], sl2, -m_ref);
+            const float p0 = q < POLY ? poly_exp2(x0) : fast_exp2(x0);
+            const float p1 = q < POLY ? poly_exp2(x1) : fast_exp2(x1);
             ps[q] += p0 + p1;
-            u[q] = pack_bf16(p0, p1);
+            pk[i0 / 2] = __uint_as_float(pack_bf16(p0, p1));
           }
-          const int kc = g * (CH / 8) + h, a = kc >> 3, cc = kc & 7;
-          *reinterpret_cast<uint4*>(prow + a * FM_TILE + ((cc ^ (r & 7)) << 4)) =
-              make_uint4(u[0], u[1], u[2], u[3]);
         }
+#pragma unroll
+        for (int c = 0; c < CH / 64; ++c) tmem_st32(prow + g * (CH / 2) + c * 32, pk + c * 32);
       }
       const float rs = (ps[0] + ps[1]) + (ps[2] + ps[3]);
       l += rs;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&p_full[buf(j)]);
+      if (lane == 0) FM_TS(warp, j, 3);
     }
     // ---------------- epilogue: O / l -> bf16 [B*L, D]
     mbar_wait(&pv_done[buf(nkb - 1)], par(nkb - 1));

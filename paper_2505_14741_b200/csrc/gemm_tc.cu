@@ -205,8 +205,12 @@ static int launch2(const TcLayer& L, const TcOperand& A, int M, int N, int K, co
 static bool use_2sm(const TcLayer& L, int precision) {
   if (precision != 1 || L.splits != 1 || g_force_2sm == 0) return false;
   if (g_force_2sm == 1) return true;
+  // waves of 256 x 256 pair tiles (74 pairs per wave; one costs ~1.6 single-SM
+  // 128 x 128 tile times, measured) against waves of 128 x 128 tiles
   const int tiles = ((L.ref_rows + TC_BM - 1) / TC_BM) * ((L.N + 127) / 128);
-  return L.ref_rows >= 2048 && tiles >= 2 * 148;
+  const int pairs = ((L.ref_rows + 255) / 256) * ((L.N + TC2_BN - 1) / TC2_BN);
+  const double w1 = (tiles + 147) / 148, w2 = (pairs + 73) / 74;
+  return L.ref_rows >= 2048 && 1.6 * w2 < w1;
 }
 
 // Tile plan. At small M the mainloop is bound by per-SM TMA ingest

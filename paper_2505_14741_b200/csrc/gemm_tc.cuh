@@ -143,6 +143,49 @@ __device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t adesc, uint64_t b
   }
 }
 
+// Warp-wide variants: every lane of the issuing warp executes them (so the
+// descriptor arithmetic stays in uniform registers) and one elected lane
+// issues the instruction.
+template <int KIND>
+__device__ __forceinline__ void umma_e(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  if constexpr (KIND == KIND_BF16) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  }
+}
+
+__device__ __forceinline__ void mbar_arrive_e(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e mbarrier.arrive.shared::cta.b64 _, [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+// (A operand read from tensor memory: tmem_a = 128 lanes x 16 bf16 = 8 columns)
+__device__ __forceinline__ void umma_ts_e(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit_e(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -406,8 +449,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tma_load_2d(st + 2 * C::A_BYTES + C::B_BYTES, &mapBlo, &full[s], kx, n0);
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer
+  } else if (warp == 1) {
+    // ---------------- MMA issuer: the whole warp runs the loop (descriptor
+    // arithmetic in uniform registers), one elected lane issues each op
     constexpr uint32_t idesc = make_idesc(KIND, TC_BM, BN);
     int seg = 0, seg_start = 0, seg_end = sk.seg[zc * G + 1] - kb0;
     for (int kb = 0; kb < nk; ++kb) {
@@ -426,7 +470,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const uint64_t a0 = smem_desc_sw128(st);
       const uint64_t b0 = smem_desc_sw128(st + C::A_BYTES);
       if (dbg & 1) {
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+        mbar_arrive_e(&empty[s]);
         continue;
       }
 #pragma unroll
@@ -434,20 +478,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // advance 32 B along K inside the swizzle atom: +2 in the >>4 address
         const uint64_t koff = (uint64_t)(k * C::UK * C::ESZ) >> 4;
         const uint32_t acc = ((kb - seg_start) | k) ? 1u : 0u;
-        umma<KIND>(dacc, a0 + koff, b0 + koff, idesc, acc);
+        umma_e<KIND>(dacc, a0 + koff, b0 + koff, idesc, acc);
         if constexpr (KIND == KIND_TF32X3) {
           const uint64_t alo = smem_desc_sw128(st + C::A_BYTES + C::B_BYTES);
           const uint64_t blo = smem_desc_sw128(st + 2 * C::A_BYTES + C::B_BYTES);
-          umma<KIND>(dacc, a0 + koff, blo + koff, idesc, 1u);
-          umma<KIND>(dacc, alo + koff, b0 + koff, idesc, 1u);
+          umma_e<KIND>(dacc, a0 + koff, blo + koff, idesc, 1u);
+          umma_e<KIND>(dacc, alo + koff, b0 + koff, idesc, 1u);
         }
       }
-      umma_commit(&empty[s]);
+      umma_commit_e(&empty[s]);
     }
     if (dbg & 1)
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(accum)) : "memory");
+      mbar_arrive_e(accum);
     else
-      umma_commit(accum);
+      umma_commit_e(accum);
   }
   __syncwarp();
 
@@ -455,7 +499,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   mbar_wait(accum, 0);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (threadIdx.x == 0) TC_STAMP(6);
-  const int row = m0 + warp * 32 + lane;
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
   if (in_cta) {
     // segments summed in order, staged per warp in the drained ring, then
@@ -631,8 +674,9 @@ static __global__ void __launch_bounds__(TC_THREADS, 1)
           "l"(reinterpret_cast<uint64_t>(&mapB)), "r"(bar), "r"(kx), "r"(nh0)
           : "memory");
     }
-  } else if (warp == 1 && lane == 0 && rank == 0) {
-    // ---------------- MMA issuer (leader): M = 256 over the pair, N = 256
+  } else if (warp == 1 && rank == 0) {
+    // ---------------- MMA issuer (leader): M = 256 over the pair, N = 256;
+    // whole warp in the loop, one elected lane issues
     constexpr uint32_t idesc = make_idesc(KIND_BF16, 256, TC2_BN);
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % TC2_STAGES;
@@ -646,19 +690,21 @@ static __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint64_t koff = (uint64_t)(k * 32) >> 4;
         const uint32_t acc = (kb | k) ? 1u : 0u;
         asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+            "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
             "l"(a0 + koff), "l"(b0 + koff), "r"(idesc), "r"(acc));
       }
       asm volatile(
-          "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-          " [%0], %1;" ::"r"(smem_u32(&empty[s])),
+          "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+          "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+          " [%0], %1;\n\t}" ::"r"(smem_u32(&empty[s])),
           "h"((uint16_t)3)
           : "memory");
     }
     asm volatile(
-        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-        " [%0], %1;" ::"r"(smem_u32(accum)),
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;\n\t}" ::"r"(smem_u32(accum)),
         "h"((uint16_t)3)
         : "memory");
   }

@@ -1,24 +1,28 @@
-// tcgen05 flash attention for long sequences, bf16 (head_dim 64).
+// tcgen05 flash attention, bf16 operands (head_dim <= 128).
 //
-// softmax(Q K^T / sqrt(dh)) V for one (lane b, head, 128-query tile) per CTA,
-// Q/K/V read by TMA straight out of the QKV GEMM's bf16 output [B*L, 3D]
-// (128-byte swizzled boxes of 128 tokens x 64 dims), scores and the output
-// accumulator in TMEM:
+// softmax(Q K^T / sqrt(dh)) V for one (lane b, head, NQ x 128-query tiles)
+// per CTA, Q/K/V read by TMA straight out of the QKV GEMM's bf16 output
+// [B*L, 3D] (128-byte swizzled boxes of 128 tokens x 64 dims); scores, the
+// bf16 probabilities and the output accumulator all live in TMEM:
 //
-//   warp 4 (1 thread)  TMA:      Q once, then K_j/V_j into a 3-stage ring
-//   warp 5 (1 thread)  MMA:      S_j = Q K_j^T  (M=128, N=128, K=64; 2 TMEM buffers)
-//                                O  += P_j V_j  (M=128, N=64,  K=128; V MN-major)
-//   warps 0-3          softmax:  thread r owns query row r (TMEM lane r):
-//                                tcgen05.ld S row -> exp2 -> P row (bf16) into
-//                                swizzled smem (the A operand of P V)
+//   TMA warp (1 lane)   Q once, then K_j/V_j into a 2-3 stage ring
+//   MMA warp (elected)  S_j = Q K_j^T  (M=128, N=128, K=DH; A, B from smem)
+//                       O  += P_j V_j  (M=128, N=DH, K=128; A = P from TMEM,
+//                                       B = V MN-major from smem)
+//   4 softmax warps     thread r owns query row r (TMEM lane r): tcgen05.ld
+//   per query tile      S row -> exp2 -> bf16 P row, tcgen05.st into TMEM
 //
-// The MMA warp issues S_{j+1} before waiting for P_j, so the score MMA of the
-// next block runs under the softmax of this one. Online softmax with a lazy
-// rescale: a row's reference max only moves when the block max exceeds it by
-// more than 2^8 (then O's row is rescaled in TMEM, after P_{j-1} V_{j-1} has
-// landed); otherwise p = exp2(s - m_ref) <= 256, exact in fp32 and safe in
-// bf16. The final O / l goes out in the proj GEMM's bf16 operand layout.
-// All reductions run in a fixed order: results do not depend on the grid.
+// The next block's scores are issued as soon as the softmax has read S out
+// of TMEM (NQ = 2: s_free, mid exp pass; NQ = 1: double-buffered S), ahead
+// of P V, so the softmax never waits on its own P V. Keeping P in TMEM takes
+// the P writes and the A-operand reads of P V off shared memory, which was
+// the tensor core's feed bottleneck. Online softmax with a lazy rescale: a
+// row's reference max only moves when the block max exceeds it by more than
+// 2^8 (then O's row is rescaled in TMEM, after P_{j-1} V_{j-1} has landed);
+// otherwise p = exp2(s - m_ref) <= 256, exact in fp32 and safe in bf16. A
+// fixed share of the exps runs on the FMA pipe (poly_exp2) to unload MUFU.
+// The final O / l goes out in the proj GEMM's bf16 operand layout. All
+// reductions run in a fixed order: results do not depend on the grid.
 #pragma once
 
 #include "attn_fmha.h"
@@ -36,11 +40,11 @@ constexpr int FM_TILE = 128 * 128;  // bytes of one 128-row x 128-byte (64 bf16)
 // DH = padded head width in smem/TMEM (64, or 128 for head_dim 72..128):
 // NA = DH/64 swizzle atoms along the head dim per Q/K/V tile.
 // NQ = 128-query tiles per CTA sharing each K/V block:
-//   NQ = 1: S double-buffered in TMEM (S0 [0,128) S1 [128,256), O [256,256+DH)),
-//           P double-buffered in smem; short sequences (more CTAs)
-//   NQ = 2: two softmax warpgroups ping-pong (tile t: S_t [128t, 128t+128),
-//           O_t [256 + 64t, ...)), one S and one P buffer per tile; the tensor
-//           core runs tile 1's MMAs under tile 0's softmax and vice versa
+//   NQ = 1: S and P double-buffered (S0 [0,128) S1 [128,256), O [256,256+DH),
+//           P0/P1 [384, 512)); short sequences (more CTAs)
+//   NQ = 2: two softmax warpgroups (tile t: S_t [128t, 128t+128), O_t
+//           [256 + 64t, ...), P_t [384 + 64t, ...)), one S and one P buffer per
+//           tile; the tensor core runs tile 1's MMAs under tile 0's softmax
 template <int DH, int NQ>
 struct FmCfg {
   static constexpr int NA = DH / 64;

@@ -32,7 +32,7 @@ static int g_fmha_poly = -1;  // test hook: exp pairs (of 4) on the polynomial (
 
 // default share of polynomial exps per configuration (measured, profiles/)
 template <int DH, int NQ>
-constexpr int fmha_poly_default() { return DH == 64 && NQ == 2 ? 1 : 0; }
+constexpr int fmha_poly_default() { return DH == 64 ? 1 : 0; }  // same for NQ = 1 and 2: bits independent of the tiling
 
 template <int DH, int NQ>
 static cudaError_t fmha_go(const CUtensorMap& map, const FmhaArgs& a, cudaStream_t st) {

@@ -387,6 +387,41 @@ def gemm_roofline(w, cfg, torch, bf16_peak):
             "launch_us": t * 1e6, "peak_note": note}
 
 
+def attn_roofline(w, cfg, bf16_peak):
+    """The tcgen05 attention kernel on one lane's full head set (device time of
+    back-to-back launches, CUDA events inside ps_attn_probe)."""
+    if cfg["spec"] is None or cfg.get("family") == "unet" or cfg["precision"] != "bf16":
+        return None
+    from paper_2505_14741_b200 import _lib
+
+    s = w.spec
+    L, H, D = s.tokens, s.heads, s.hidden
+    iters = 3 if L > 8192 else 50
+    lib = _lib.load()
+    lib.ps_attn_probe(1, L, H, D, 2, 1)
+    us = lib.ps_attn_probe(1, L, H, D, 2, iters)
+    flops = 4.0 * L * L * (D // H) * H
+    achieved = flops / (us * 1e-6) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(f"{cfg['spec']}_{cfg['precision']}_attn")
+    return {"bound": "tensor", "achieved": achieved, "peak": bf16_peak, "unit": "TFLOP/s",
+            "frac": achieved / bf16_peak, "traffic": traffic,
+            "kernel": f"fmha_tc L={L} heads={H} head_dim={D // H} (bf16)", "launch_us": us,
+            "peak_note": "measured bf16 dense (burst); MUFU ex2 bounds head_dim 64 at ~1/2 of it"}
+
+
+def dominant_is_attention(w, cfg):
+    """Per-forward FLOPs: attention 4 L^2 D vs the block GEMMs 2 L (4 D^2 + 2 D F)."""
+    if cfg["spec"] is None or cfg.get("family") == "unet":
+        return False
+    s = w.spec
+    L, D = s.tokens, s.hidden
+    return 4.0 * L * L * D > 2.0 * L * (4 * D * D + 2 * D * s.mlp_hidden)
+
+
 def sched_roofline(torch, hbm_peak):
     """The fused apply kernel on an HBM-sized vector (8 apply steps, fp32)."""
     from paper_2505_14741_b200 import _lib
@@ -479,6 +514,9 @@ def our_arm(args, cfg, world, rank, local):
     d2h = ((2 * cfg["T"] + 1) * n * es) if rank == 0 else n * es
 
     roof = gemm_roofline(w, cfg, torch, bf16_peak) if rank == 0 else None
+    roof_attn = attn_roofline(w, cfg, bf16_peak) if rank == 0 else None
+    if roof_attn is not None and dominant_is_attention(w, cfg):
+        roof, roof_attn = roof_attn, roof  # the attention kernel dominates the step
     roof_sched = sched_roofline(torch, hbm_peak) if rank == 0 else None
 
     extra = {}
@@ -529,6 +567,7 @@ def our_arm(args, cfg, world, rank, local):
         "launches_per_denoise": launches,
         "roofline": roof,
         "roofline_sched": roof_sched,
+        "roofline_other": roof_attn,
         "peaks_source": peak_src,
         "cpu_baseline": cpu,
         "rel_mae_vs_reference": rel,

@@ -15,6 +15,8 @@ WANT = [
     ("sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active", "hmma_pct", 1),
     ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor_pct", 1),
     ("sm__inst_executed_pipe_uma.avg.pct_of_peak_sustained_active", "uma_pct", 1),
+    ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "xu_pct", 1),
+    ("sm__issue_active.avg.pct_of_peak_sustained_active", "issue_pct", 1),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm_pct", 1),
     ("gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed", "mem_pct", 1),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram_pct", 1),

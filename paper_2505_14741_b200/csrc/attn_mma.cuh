@@ -505,6 +505,27 @@ __global__ void __launch_bounds__(KW * 32) attn_ks_kernel(const __grid_constant_
     }
   }
   __syncthreads();
+  // per-row merge weights f_w = exp(m_w - M) and denominators, once per row
+  // (not once per output element), same operations in the same order
+  float* fs = os + (size_t)KW * FA_QW * DHP;  // [KW][16]
+  float* dens = fs + KW * FA_QW;              // [16]
+  if (threadIdx.x < FA_QW) {
+    const int r = threadIdx.x;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < KW; ++w) M = fmaxf(M, ms[w * FA_QW + r]);
+    float den = 0.f;
+#pragma unroll
+    for (int w = 0; w < KW; ++w) {
+      const float mw = ms[w * FA_QW + r];
+      const float f = mw == -INFINITY ? 0.f
+                                      : (MODE == AM_BF16 ? exp2f(mw - M) : expf(mw - M));
+      fs[w * FA_QW + r] = f;
+      den = fmaf(ls[w * FA_QW + r], f, den);
+    }
+    dens[r] = den;
+  }
+  __syncthreads();
   LnModArgs st{};
   st.out_f32 = p.out_f32;
   st.out_bf16 = p.out_bf16;
@@ -513,19 +534,11 @@ __global__ void __launch_bounds__(KW * 32) attn_ks_kernel(const __grid_constant_
   for (int idx = threadIdx.x; idx < FA_QW * dh; idx += KW * 32) {
     const int r = idx / dh, d = idx % dh, q = q0 + r;
     if (q >= L) continue;
-    float M = -INFINITY;
+    float num = 0.f;
 #pragma unroll
-    for (int w = 0; w < KW; ++w) M = fmaxf(M, ms[w * FA_QW + r]);
-    float num = 0.f, den = 0.f;
-#pragma unroll
-    for (int w = 0; w < KW; ++w) {
-      const float mw = ms[w * FA_QW + r];
-      const float f = mw == -INFINITY ? 0.f
-                                      : (MODE == AM_BF16 ? exp2f(mw - M) : expf(mw - M));
-      num = fmaf(os[((size_t)w * FA_QW + r) * DHP + d], f, num);
-      den = fmaf(ls[w * FA_QW + r], f, den);
-    }
-    store_act(st, (row0 + q) * p.D + head * dh + d, num / den);
+    for (int w = 0; w < KW; ++w)
+      num = fmaf(os[((size_t)w * FA_QW + r) * DHP + d], fs[w * FA_QW + r], num);
+    store_act(st, (row0 + q) * p.D + head * dh + d, num / dens[r]);
   }
 }
 

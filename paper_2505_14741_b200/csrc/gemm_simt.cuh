@@ -52,10 +52,16 @@ __device__ __forceinline__ int64_t padded_index(const Epi& e, int m, int n, int 
   return (int64_t)m * (N / e.pad_dh * e.pad_DH) + (n / e.pad_dh) * e.pad_DH + n % e.pad_dh;
 }
 
+// GELU of an epilogue: MUFU tanh when the only output is bf16, the accurate
+// tanhf whenever an fp32 (or tf32 hi/lo) value leaves the kernel
+__device__ __forceinline__ float epi_gelu(const Epi& e, float v) {
+  return (e.out_bf16 && !e.out && !e.out_hi) ? gelu_tanh_fast(v) : gelu_tanh_f(v);
+}
+
 __device__ __forceinline__ float epi_add_val(const Epi& e, int m, int n, int64_t idx, float v) {
   if (e.vec) v += e.vec[lane_row(e, m) * e.vec_stride + n];
   if (e.resid) v += e.resid[idx];
-  return e.act ? gelu_tanh_f(v) : v;
+  return e.act ? epi_gelu(e, v) : v;
 }
 
 __device__ __forceinline__ void epi_store(const Epi& e, int m, int n, int N, float acc) {
@@ -67,7 +73,7 @@ __device__ __forceinline__ void epi_store(const Epi& e, int m, int n, int N, flo
       if (e.out_bf16) e.out_bf16[e.pad_DH ? padded_index(e, m, n, N) : idx] = __float2bfloat16_rn(v);
       break;
     case EPI_GELU: {
-      const float g = gelu_tanh_f(v);
+      const float g = epi_gelu(e, v);
       if (e.out) e.out[idx] = g;
       if (e.out_bf16) e.out_bf16[idx] = __float2bfloat16_rn(g);
       if (e.out_hi) {
@@ -143,7 +149,7 @@ __device__ __forceinline__ void epi_store16(const Epi& e, int m, int n, int N, c
     }
   } else if (e.mode == EPI_GELU) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) x[j] = gelu_tanh_f(x[j]);
+    for (int j = 0; j < 16; ++j) x[j] = epi_gelu(e, x[j]);
     if (e.out)
 #pragma unroll
       for (int q = 0; q < 4; ++q)
@@ -188,7 +194,7 @@ __device__ __forceinline__ void epi_store16(const Epi& e, int m, int n, int N, c
     }
     if (e.act)
 #pragma unroll
-      for (int j = 0; j < 16; ++j) x[j] = gelu_tanh_f(x[j]);
+      for (int j = 0; j < 16; ++j) x[j] = epi_gelu(e, x[j]);
     if (e.out)
 #pragma unroll
       for (int q = 0; q < 4; ++q)
@@ -248,7 +254,7 @@ __device__ __forceinline__ void epi_store4(const Epi& e, int m, int n, int N, co
     if (e.out_bf16) st_bf16(e.out_bf16);
   } else if (e.mode == EPI_GELU) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) x[j] = gelu_tanh_f(x[j]);
+    for (int j = 0; j < 4; ++j) x[j] = epi_gelu(e, x[j]);
     if (e.out) st_f32(e.out);
     if (e.out_bf16) st_bf16(e.out_bf16);
     if (e.out_hi) {
@@ -268,7 +274,7 @@ __device__ __forceinline__ void epi_store4(const Epi& e, int m, int n, int N, co
     }
     if (e.act)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) x[j] = gelu_tanh_f(x[j]);
+      for (int j = 0; j < 4; ++j) x[j] = epi_gelu(e, x[j]);
     if (e.out) st_f32(e.out);
     if (e.out_bf16) st_bf16(e.out_bf16);
   } else {  // EPI_RESID

@@ -132,7 +132,8 @@ static int launch(const TcLayer& L, const TcOperand& A, int M, int N, int K, con
     const size_t ring = (size_t)C::STAGES * C::STAGE_BYTES;
     const size_t ptile = (size_t)TC_BM * (BN + 4) * sizeof(float);
     for (int c = L.splits < g_sc_max ? L.splits : g_sc_max; c > 1; c /= 2) {
-      if (tiles * c <= cluster_cap(c) && (size_t)(L.splits / c) * ptile <= ring) {
+      // the CTA's partial tiles plus its reduced slab (128 / c rows) in the drained ring
+      if (tiles * c <= cluster_cap(c) && (size_t)(L.splits / c) * ptile + ptile / c <= ring) {
         sc = c;
         break;
       }
@@ -444,14 +445,18 @@ float ps_gemm_probe(int M, int N, int K, int precision, int dbg, int iters) {
   g_split_enable = (dbg & 32) ? 0 : 1;  // bit 5: disable split-K
   g_force_in_cta = (dbg & 64) ? 1 : 0;  // bit 6: segments in-CTA
   const bool resid_epi = (dbg & 1024) != 0;  // bit 10: gated-residual epilogue (EPI_RESID)
+  const bool gelu_epi = (dbg & 4096) != 0;   // bit 12: GELU epilogue, next GEMM's operand format
+  const bool nonzero = (dbg & 8192) != 0;    // bit 13: operands 0x3c3c3c3c (~0.0115), not 0
   g_force_2sm = (dbg & 2048) ? 0 : -1;       // bit 11: never the 2-SM kernel
   dbg &= 31;
   float *A = nullptr, *W = nullptr, *C = nullptr;
   if (cudaMalloc(&A, (size_t)M * K * 4) || cudaMalloc(&W, (size_t)K * N * 4) ||
       cudaMalloc(&C, (size_t)M * N * 4))
     return -1.f;
-  cudaMemset(A, 0, (size_t)M * K * 4);
-  cudaMemset(W, 0, (size_t)K * N * 4);
+  cudaMemset(A, nonzero ? 0x3c : 0, (size_t)M * K * 4);
+  cudaMemset(W, nonzero ? 0x3c : 0, (size_t)K * N * 4);
+  float* C2 = nullptr;
+  if (gelu_epi && cudaMalloc(&C2, (size_t)M * N * 4)) return -1.f;
   TcWeights w;
   TcActs acts;
   std::vector<const float*> Ws{W};
@@ -470,6 +475,16 @@ float ps_gemm_probe(int M, int N, int K, int precision, int dbg, int iters) {
       e.gate = ones;
       e.gate_stride = 0;
       e.L = M;
+    }
+    if (gelu_epi) {
+      e.mode = EPI_GELU;
+      e.out = nullptr;
+      if (precision == 0) {
+        e.out_hi = C;
+        e.out_lo = C2;
+      } else {
+        e.out_bf16 = reinterpret_cast<__nv_bfloat16*>(C);
+      }
     }
     cudaEvent_t a, b;
     cudaEventCreate(&a);
@@ -493,6 +508,7 @@ float ps_gemm_probe(int M, int N, int K, int precision, int dbg, int iters) {
   cudaFree(A);
   cudaFree(W);
   cudaFree(C);
+  if (C2) cudaFree(C2);
   g_split_enable = 1;
   g_force_in_cta = 0;
   g_force_2sm = -1;

@@ -19,6 +19,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <type_traits>
 #include <vector>
 
 #include "gemm_simt.cuh"
@@ -274,7 +275,7 @@ __device__ __forceinline__ void cluster_sync_all() {
 // residual epilogue at CogVideoX shape, where the residual stream exceeds L2.
 template <int NC, int EST>
 __device__ __forceinline__ void warp_store_rows(const Epi& e, const float* stg, int row0, int col0,
-                                                int M, int N, int lane) {
+                                                int M, int N, int lane, int nrows = 32) {
   static_assert(NC % 4 == 0 && NC <= 128, "one float4 column group per lane and row");
   constexpr int LPR = NC / 4 < 32 ? NC / 4 : 32;  // lanes per row
   constexpr int RPP = 32 / LPR;                   // rows per pass
@@ -290,13 +291,13 @@ __device__ __forceinline__ void warp_store_rows(const Epi& e, const float* stg, 
                              : make_float4(0.f, 0.f, 0.f, 0.f);
     const bool resid_mode = e.mode == EPI_RESID;
 #pragma unroll 1
-    for (int r0 = 0; r0 < 32; r0 += RPP * RB) {
+    for (int r0 = 0; r0 < nrows; r0 += RPP * RB) {
       float4 ga[RB], rb[RB];
 #pragma unroll
       for (int i = 0; i < RB; ++i) {
         const int r = r0 + i * RPP + lane / LPR, grow = row0 + r;
         ga[i] = rb[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (grow >= M) continue;
+        if (grow >= M || r >= nrows) continue;
         const int64_t base = (int64_t)grow * N + col;
         if (resid_mode)
           ga[i] = *reinterpret_cast<const float4*>(e.gate + lane_row(e, grow) * e.gate_stride + col);
@@ -307,7 +308,7 @@ __device__ __forceinline__ void warp_store_rows(const Epi& e, const float* stg, 
 #pragma unroll
       for (int i = 0; i < RB; ++i) {
         const int r = r0 + i * RPP + lane / LPR, grow = row0 + r;
-        if (grow >= M) continue;
+        if (grow >= M || r >= nrows) continue;
         const int64_t base = (int64_t)grow * N + col;
         const float4 a = *reinterpret_cast<const float4*>(stg + r * EST + c4);
         float x[4] = {a.x + bb.x, a.y + bb.y, a.z + bb.z, a.w + bb.w};
@@ -329,7 +330,7 @@ __device__ __forceinline__ void warp_store_rows(const Epi& e, const float* stg, 
         }
         if (e.act)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) x[j] = gelu_tanh_f(x[j]);
+          for (int j = 0; j < 4; ++j) x[j] = epi_gelu(e, x[j]);
         if (e.out)
           *reinterpret_cast<float4*>(e.out + base) = make_float4(x[0], x[1], x[2], x[3]);
         if (e.out_bf16) {
@@ -343,16 +344,24 @@ __device__ __forceinline__ void warp_store_rows(const Epi& e, const float* stg, 
     }
     return;
   }
-#pragma unroll 1
-  for (int r0 = 0; r0 < 32; r0 += RPP) {
+  auto row_pass = [&](int r0) {
     const int r = r0 + lane / LPR, grow = row0 + r;
-    if (grow >= M) continue;
+    if (grow >= M || r >= nrows) return;
     for (int c4 = (lane % LPR) * 4; c4 < NC; c4 += LPR * 4) {
       if (col0 + c4 >= N) break;
       const float4 a = *reinterpret_cast<const float4*>(stg + r * EST + c4);
       const float v[4] = {a.x, a.y, a.z, a.w};
       epi_store4(e, grow, col0 + c4, N, v);
     }
+  };
+  // plain stores gain from 4 rows in flight (measured: 5% at CogVideoX
+  // shapes); the GELU modes lose from it (register pressure)
+  if (e.mode == EPI_STORE) {
+#pragma unroll 4
+    for (int r0 = 0; r0 < nrows; r0 += RPP) row_pass(r0);
+  } else {
+#pragma unroll 1
+    for (int r0 = 0; r0 < nrows; r0 += RPP) row_pass(r0);
   }
 }
 
@@ -547,34 +556,55 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // same order as the in-CTA path, one float4 per thread per pass
     const int rows = TC_BM / SC, r0 = zc * rows;
     const int chunks = rows * (BN / 4);
-    // two float4 chunks per thread per pass: 2 x S remote loads in flight
-    for (int base = threadIdx.x; base < chunks; base += 2 * TC_THREADS) {
-      float4 a[2][8];
+    float* red = part + G * PTILE;  // this CTA's reduced rows [rows][PST], then the epilogue
+    // SS segments: 16 / SS float4 chunks per thread per pass, every remote
+    // load of a pass issued before the first use (DSMEM latency is what this
+    // phase costs; 2 chunks per pass left it latency-bound)
+    auto reduce = [&](auto seg_tag) {
+      constexpr int SS = decltype(seg_tag)::value;
+      constexpr int U = SS >= 16 ? 1 : 16 / SS;
+      for (int base = threadIdx.x; base < chunks; base += U * TC_THREADS) {
+        float4 a[U][SS];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int idx = base + u * TC_THREADS;
-        if (idx >= chunks) break;
-        const int r = r0 + idx / (BN / 4), c = (idx % (BN / 4)) * 4;
-        const float* src = part + r * PST + c;
+        for (int u = 0; u < U; ++u) {
+          const int idx = base + u * TC_THREADS;
+          if (idx >= chunks) break;
+          const int r = r0 + idx / (BN / 4), c = (idx % (BN / 4)) * 4;
+          const float* src = part + r * PST + c;
 #pragma unroll
-        for (int sg = 0; sg < 8; ++sg)
-          if (sg < S)
+          for (int sg = 0; sg < SS; ++sg)
             a[u][sg] = G == 1 ? ld_dsmem_f4(src, (uint32_t)sg)
                               : ld_dsmem_f4(src + (sg % G) * PTILE, (uint32_t)(sg / G));
-      }
+        }
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int idx = base + u * TC_THREADS;
-        if (idx >= chunks) break;
-        const int r = r0 + idx / (BN / 4), c = (idx % (BN / 4)) * 4;
-        float v[4] = {a[u][0].x, a[u][0].y, a[u][0].z, a[u][0].w};
+        for (int u = 0; u < U; ++u) {
+          const int idx = base + u * TC_THREADS;
+          if (idx >= chunks) break;
+          const int r = r0 + idx / (BN / 4), c = (idx % (BN / 4)) * 4;
+          float4 v = a[u][0];
 #pragma unroll
-        for (int sg = 1; sg < 8; ++sg)
-          if (sg < S) {
-            v[0] += a[u][sg].x; v[1] += a[u][sg].y; v[2] += a[u][sg].z; v[3] += a[u][sg].w;
+          for (int sg = 1; sg < SS; ++sg) {
+            v.x += a[u][sg].x; v.y += a[u][sg].y; v.z += a[u][sg].z; v.w += a[u][sg].w;
           }
-        if (m0 + r < M && n0 + c < N) epi_store4(e, m0 + r, n0 + c, N, v);
+          *reinterpret_cast<float4*>(red + (r - r0) * PST + c) = v;
+        }
       }
+    };
+    switch (S) {
+      case 2: reduce(std::integral_constant<int, 2>{}); break;
+      case 3: reduce(std::integral_constant<int, 3>{}); break;
+      case 4: reduce(std::integral_constant<int, 4>{}); break;
+      case 5: reduce(std::integral_constant<int, 5>{}); break;
+      case 6: reduce(std::integral_constant<int, 6>{}); break;
+      case 7: reduce(std::integral_constant<int, 7>{}); break;
+      default: reduce(std::integral_constant<int, 8>{}); break;
+    }
+    __syncthreads();
+    {  // coalesced epilogue over the reduced slab: rows / 4 rows per warp
+      const int rpw = rows / 4;
+      if ((dbg & 4) == 0)
+        warp_store_rows<BN, PST>(e, red + warp * rpw * PST, m0 + r0 + warp * rpw, n0, M, N, lane,
+                                 rpw);
     }
     if (threadIdx.x == 0) TC_STAMP(11);
     cluster_sync_all();  // peers' smem stays live until every CTA has read it

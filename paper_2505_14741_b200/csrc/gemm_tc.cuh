@@ -266,6 +266,11 @@ __device__ __forceinline__ void cluster_sync_all() {
                    : "memory");
 }
 
+// DSMEM split-K reduction: float4 loads in flight per thread per pass
+// (measured 4 / 8 / 16: 4 best end to end - DiT-S 38.7 vs 39.7 ms, U-Net
+// 709 vs 728 / 746 ms; profiles/r1d_epilogue_variants.txt)
+constexpr int TC_REDUCE_LOADS = 4;
+
 // Coalesced epilogue for one warp's 32 accumulator rows x NC columns that the
 // warp has staged row-major in smem (stride EST floats): written back row by
 // row with consecutive lanes on consecutive 4-column groups, so every store
@@ -557,12 +562,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int rows = TC_BM / SC, r0 = zc * rows;
     const int chunks = rows * (BN / 4);
     float* red = part + G * PTILE;  // this CTA's reduced rows [rows][PST], then the epilogue
-    // SS segments: 16 / SS float4 chunks per thread per pass, every remote
-    // load of a pass issued before the first use (DSMEM latency is what this
-    // phase costs; 2 chunks per pass left it latency-bound)
+    // gated residual / GELU: through the slab (coalesced rows, batched
+    // residual loads); the other modes store straight from registers (the
+    // slab measured slower for the U-Net's add / store epilogues)
+    const bool slab = e.mode == EPI_RESID || e.mode == EPI_GELU;
+    // SS segments: TC_REDUCE_LOADS / SS float4 chunks per thread per pass,
+    // every remote load of a pass issued before the first use
     auto reduce = [&](auto seg_tag) {
       constexpr int SS = decltype(seg_tag)::value;
-      constexpr int U = SS >= 16 ? 1 : 16 / SS;
+      constexpr int U = SS >= TC_REDUCE_LOADS ? 1 : TC_REDUCE_LOADS / SS;
       for (int base = threadIdx.x; base < chunks; base += U * TC_THREADS) {
         float4 a[U][SS];
 #pragma unroll
@@ -586,7 +594,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           for (int sg = 1; sg < SS; ++sg) {
             v.x += a[u][sg].x; v.y += a[u][sg].y; v.z += a[u][sg].z; v.w += a[u][sg].w;
           }
-          *reinterpret_cast<float4*>(red + (r - r0) * PST + c) = v;
+          if (slab) {
+            *reinterpret_cast<float4*>(red + (r - r0) * PST + c) = v;
+          } else if (m0 + r < M && n0 + c < N) {
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+            epi_store4(e, m0 + r, n0 + c, N, vv);
+          }
         }
       }
     };
@@ -599,8 +612,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       case 7: reduce(std::integral_constant<int, 7>{}); break;
       default: reduce(std::integral_constant<int, 8>{}); break;
     }
-    __syncthreads();
-    {  // coalesced epilogue over the reduced slab: rows / 4 rows per warp
+    if (slab) {  // coalesced epilogue over the reduced slab: rows / 4 rows per warp
+      __syncthreads();
       const int rpw = rows / 4;
       if ((dbg & 4) == 0)
         warp_store_rows<BN, PST>(e, red + warp * rpw * PST, m0 + r0 + warp * rpw, n0, M, N, lane,

@@ -242,6 +242,11 @@ int ps_peer_wait(const uint64_t* ready, int count, const uint64_t* base, uint64_
 int ps_peer_epoch_advance(uint64_t* base, void* cuda_stream);
 /* async device-to-device (or peer) copy on the stream */
 int ps_copy(void* dst, const void* src, size_t bytes, void* cuda_stream);
+/* Writes the GPU's %globaltimer (ns) to *slot when the stream reaches it:
+ * phase stamps for the per-rank forward / exchange-wait / apply split that
+ * replaces the reference's WorkerTimings (pkg/src/parastep/protocol/
+ * worker.py:65-85, loop_latency_s :108-110). */
+int ps_stamp(uint64_t* slot, void* cuda_stream);
 
 /* ---- trajectory files and diagnostics on device --------
  * ps_traj_pack writes the reference's binary trajectory file

@@ -110,6 +110,7 @@ _SIGS = {
     "ps_peer_wait": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64, C.c_void_p]),
     "ps_peer_epoch_advance": (C.c_int, [C.c_void_p, C.c_void_p]),
     "ps_copy": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "ps_stamp": (C.c_int, [C.c_void_p, C.c_void_p]),
     "ps_traj_pack_bytes": (C.c_int64, [C.c_int, C.c_int64]),
     "ps_traj_pack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                C.c_void_p, C.c_int, C.c_int64, C.c_int, C.c_void_p, C.c_void_p]),

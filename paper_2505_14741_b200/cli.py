@@ -191,11 +191,13 @@ def cmd_compare(ns) -> int:
             else:
                 s = DeviceSampler(w, sched, _cfg(ns, w, ns.seed + i, warmup, name, d))
                 s.run(ns.seed + i)
-            rows, x0 = compare_trajectories_device(refs[i], s)
+            report = compare_trajectories_device(refs[i], s)
+            # the strategy's own adjacent-step series (T-1 rows, cli.py:530-535)
             adjacent += [f"{label},{ns.seed + i},{r.t},{_f(r.rel_mae_x)},{_f(r.rel_mae_eps)}"
-                         for r in rows]
-            divergence.append(f"{label},{ns.seed + i},{_f(x0)},{_f(rows[-1].mse_x)}")
-            finals[label].append(x0)
+                         for r in report.adjacent_b]
+            divergence.append(f"{label},{ns.seed + i},{_f(report.final_rel_mae)},"
+                              f"{_f(report.final_mse)}")
+            finals[label].append(report.final_rel_mae)
     (out / "adjacent.csv").write_text("\n".join(adjacent) + "\n")
     (out / "divergence.csv").write_text("\n".join(divergence) + "\n")
     summary = ["command=compare", f"seeds={ns.seeds}", f"steps={ns.steps}", f"warmup={warmup}"]

@@ -291,13 +291,9 @@ int ps_dit_condition_reserve(ps_dit* h, int T) {
       return rc;
   }
   if (T + 1 > h->cond_cap) {
-    if (h->cond) {  // owned list keeps the old block; release it now
-      for (auto& p : h->owned)
-        if (p == h->cond) {
-          cudaFree(p);
-          p = nullptr;
-        }
-    }
+    // grow only; the smaller block stays in the owned list until destroy: a
+    // CUDA graph captured by another sampler on these weights still holds
+    // its address (its forwards and conditioning launches read it)
     if (int rc = dalloc_t(h, &h->cond, (size_t)(T + 1) * h->n_ada)) return rc;
     h->cond_cap = T + 1;
   }

@@ -54,6 +54,15 @@ static __global__ void peer_wait_kernel(const uint64_t* ready, int count, const 
 
 static __global__ void peer_epoch_kernel(uint64_t* base) { *base += 1ull << 20; }
 
+// Device phase stamp for the per-rank forward / exchange-wait / apply split
+// (the reference's WorkerTimings, protocol/worker.py:65-85): the GPU's
+// nanosecond global timer, written when the stream reaches this point.
+static __global__ void stamp_kernel(uint64_t* slot) {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *slot = t;
+}
+
 }  // namespace ps
 
 using namespace ps;
@@ -120,6 +129,12 @@ int ps_peer_epoch_advance(uint64_t* base, void* cs) {
   PS_CHECK_ARG(base, "null epoch");
   peer_epoch_kernel<<<1, 1, 0, as_stream(cs)>>>(base);
   return check_launch("peer_epoch");
+}
+
+int ps_stamp(uint64_t* slot, void* cs) {
+  PS_CHECK_ARG(slot, "null stamp slot");
+  stamp_kernel<<<1, 1, 0, as_stream(cs)>>>(slot);
+  return check_launch("stamp");
 }
 
 }  // extern "C"

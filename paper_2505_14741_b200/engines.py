@@ -587,47 +587,100 @@ class DiffRow:
     mse_eps: float
 
 
-def compare_trajectories(a: Trajectory, b: Trajectory):
-    """Per-step divergence of b from reference a (engines.py:446-473, rows + final)."""
+@dataclass
+class AdjacentRow:
+    t: int
+    rel_mae_x: float
+    rel_mae_eps: float
+
+
+def _adjacent_series(traj: Trajectory) -> list[AdjacentRow]:
+    """rel_mae(value_t, value_{t+1}) of consecutive records (engines.py:422-428)."""
+    return [AdjacentRow(cur.t, rel_mae(cur.x, prev.x), rel_mae(cur.eps, prev.eps))
+            for prev, cur in zip(traj.records, traj.records[1:])]
+
+
+@dataclass
+class DiffReport:
+    """engines.py:431-443: per-step rows, final x0 rel-MAE / MSE, and the
+    adjacent-step self-similarity series of both trajectories (T-1 rows)."""
+
+    rows: list[DiffRow]
+    final_rel_mae: float
+    final_mse: float
+    adjacent_a: list[AdjacentRow]
+    adjacent_b: list[AdjacentRow]
+
+    def to_csv(self) -> str:
+        lines = ["step,rel_mae_x,rel_mae_eps,mse_x,mse_eps"]
+        for r in self.rows:
+            lines.append(f"{r.t},{r.rel_mae_x!r},{r.rel_mae_eps!r},{r.mse_x!r},{r.mse_eps!r}")
+        return "\n".join(lines) + "\n"
+
+
+def compare_trajectories(a: Trajectory, b: Trajectory) -> DiffReport:
+    """Per-step divergence of b from reference a (engines.py:446-473)."""
     if len(a.records) != len(b.records):
         raise DimensionError(f"trajectory lengths differ: {len(a.records)} vs {len(b.records)}")
+    if len(a.x0) != len(b.x0):
+        raise DimensionError(f"data dims differ: {len(a.x0)} vs {len(b.x0)}")
     rows = []
     for ra, rb in zip(a.records, b.records):
         if ra.t != rb.t:
             raise DimensionError(f"step mismatch: {ra.t} vs {rb.t}")
         rows.append(DiffRow(ra.t, rel_mae(ra.x, rb.x), rel_mae(ra.eps, rb.eps), mse(ra.x, rb.x),
                             mse(ra.eps, rb.eps)))
-    return rows, rel_mae(a.x0, b.x0)
+    return DiffReport(rows, rel_mae(a.x0, b.x0), mse(a.x0, b.x0), _adjacent_series(a),
+                      _adjacent_series(b))
 
 
-def compare_trajectories_device(a: "DeviceSampler", b: "DeviceSampler"):
+def compare_trajectories_device(a: "DeviceSampler", b: "DeviceSampler") -> DiffReport:
     """compare_trajectories of two samplers' last runs without leaving the GPU.
 
-    Same rows (t, rel-MAE / MSE of x and eps, a = reference) and final x0
-    rel-MAE as ``compare_trajectories`` (engines.py:446-473); the sums run on
-    device in fp64 with a fixed reduction order (``ps_traj_diff``), so they
-    agree with the host's left-to-right sums to rounding (~1e-15 relative).
+    The same DiffReport as ``compare_trajectories`` (engines.py:446-473): the
+    per-step rows (a = reference), the final x0 rel-MAE and MSE, and both
+    adjacent-step series. All sums run on device in fp64 with a fixed
+    reduction order (``ps_traj_diff``), so they agree with the host's
+    left-to-right sums to rounding (~1e-15 relative).
     """
     import torch
 
-    if a.T != b.T or a.n != b.n:
-        raise DimensionError(f"trajectory shapes differ: {a.T}x{a.n} vs {b.T}x{b.n}")
+    if a.T != b.T:
+        raise DimensionError(f"trajectory lengths differ: {a.T} vs {b.T}")
+    if a.n != b.n:
+        raise DimensionError(f"data dims differ: {a.n} vs {b.n}")
     if not (a.record and b.record):
         raise ConfigError("both samplers need per-step x records")
     lib = _lib.load(require_gpu=True)
     T, n = a.T, a.n
-    out = torch.empty((2 * T + 1, 3), dtype=torch.float64, device="cuda")
-    ra = torch.tensor(a.src_row, dtype=torch.int32, device="cuda")
-    rb = torch.tensor(b.src_row, dtype=torch.int32, device="cuda")
+    # rows: [0,T) x diff, [T,2T) eps diff, 2T x0, then the adjacent series of a
+    # and b: (T-1) x rows + (T-1) eps rows each
+    nrow = 2 * T + 1 + 4 * max(T - 1, 0)
+    out = torch.empty((nrow, 3), dtype=torch.float64, device="cuda")
+    ar = list(range(T))
+    idx = torch.tensor([ar, list(a.src_row), list(b.src_row)], dtype=torch.int32, device="cuda")
     st = _lib.stream_ptr()
-    _lib.check(lib.ps_traj_diff(_lib.ptr(a.rec_x), _lib.ptr(b.rec_x), None, None, T, n,
-                                a.dtype_code, b.dtype_code, _lib.ptr(out), st), "traj_diff")
-    _lib.check(lib.ps_traj_diff(_lib.ptr(a.eps), _lib.ptr(b.eps), _lib.ptr(ra), _lib.ptr(rb), T, n,
-                                a.dtype_code, b.dtype_code, _lib.ptr(out) + 3 * T * 8, st),
-               "traj_diff")
-    _lib.check(lib.ps_traj_diff(_lib.ptr(a.x0_device), _lib.ptr(b.x0_device), None, None, 1, n,
-                                a.dtype_code, b.dtype_code, _lib.ptr(out) + 6 * T * 8, st),
-               "traj_diff")
+    ptr = _lib.ptr
+
+    def diff(x, y, rx, ry, rows, row0, dx, dy):
+        _lib.check(lib.ps_traj_diff(ptr(x), ptr(y), rx, ry, rows, n, dx, dy,
+                                    ptr(out) + 3 * row0 * 8, st), "traj_diff")
+
+    def irow(which, start):
+        return ptr(idx) + (which * T + start) * 4
+
+    diff(a.rec_x, b.rec_x, None, None, T, 0, a.dtype_code, b.dtype_code)
+    diff(a.eps, b.eps, irow(1, 0), irow(2, 0), T, T, a.dtype_code, b.dtype_code)
+    diff(a.x0_device, b.x0_device, None, None, 1, 2 * T, a.dtype_code, b.dtype_code)
+    if T > 1:
+        base = 2 * T + 1
+        for s_i, (smp, which) in enumerate(((a, 1), (b, 2))):
+            r0 = base + s_i * 2 * (T - 1)
+            # cur = record k+1 (reference side of rel_mae), prev = record k
+            diff(smp.rec_x, smp.rec_x, irow(0, 1), irow(0, 0), T - 1, r0, smp.dtype_code,
+                 smp.dtype_code)
+            diff(smp.eps, smp.eps, irow(which, 1), irow(which, 0), T - 1, r0 + T - 1,
+                 smp.dtype_code, smp.dtype_code)
     s = out.cpu().numpy()
 
     def rel(row):
@@ -637,4 +690,9 @@ def compare_trajectories_device(a: "DeviceSampler", b: "DeviceSampler"):
 
     rows = [DiffRow(T - k, rel(s[k]), rel(s[T + k]), s[k][2] / n, s[T + k][2] / n)
             for k in range(T)]
-    return rows, rel(s[2 * T])
+    adj = []
+    for s_i in range(2):
+        r0 = 2 * T + 1 + s_i * 2 * (T - 1)
+        adj.append([AdjacentRow(T - (k + 1), rel(s[r0 + k]), rel(s[r0 + T - 1 + k]))
+                    for k in range(T - 1)])
+    return DiffReport(rows, rel(s[2 * T]), s[2 * T][2] / n, adj[0], adj[1])

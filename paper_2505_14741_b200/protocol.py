@@ -28,6 +28,7 @@ from dataclasses import dataclass, field
 
 from . import _lib
 from .engines import (
+    STRATEGY_DYNAMIC,
     STRATEGY_PARASTEP,
     RunConfig,
     StepRecord,
@@ -37,6 +38,7 @@ from .engines import (
     plan_cycles,
 )
 from .errors import ConfigError, ProtocolAbortError
+from .ledger import ExchangeLedger
 from .numerics import PURPOSE_INIT, stream_id
 from .schedule import NoiseSchedule, step_coeffs
 
@@ -47,34 +49,95 @@ def rank_loop(ops, T: int, warmup: int, p: int, rank: int, cycles: list[list[int
     ops.init() -> x; ops.forward(x, t, slot) -> eps; ops.zeros(slot) -> eps;
     ops.allgather(eps) -> list of p eps; ops.apply_roll(x, apply_ts, eps_list,
     roll_ts, cache) -> (x, lane_x) with roll_ts == [] meaning no roll.
-    ops.record(k, eps) optionally stores trajectory eps rows.
+    ops.record(k, eps) optionally stores trajectory eps rows. Optional hooks:
+    ops.stamp(tag) marks phase boundaries (forward / exchange / apply, the
+    reference's WorkerTimings, worker.py:65-85) and ops.finish() closes the
+    run (the peer exchange's end-of-run handshake).
     """
+    stamp = getattr(ops, "stamp", None) or (lambda tag: None)
     x = ops.init()
+    stamp("start")
     lane_x = None
     cache = None
     warm_ts = list(range(T, T - warmup, -1))
     for i, t in enumerate(warm_ts):
+        stamp("fwd0")
         e = ops.forward(x, t, "warm")
+        stamp("fwd1")
         ops.record(T - t, [e])
         nxt = cycles[0] if (i == len(warm_ts) - 1 and cycles) else None
         roll = nxt[:rank] if (nxt is not None and 1 <= rank < len(nxt)) else []
         cache = e
         x, lane_x = ops.apply_roll(x, [t], [e], roll, cache)
+        stamp("apply")
     for ci, cyc in enumerate(cycles):
         c = len(cyc)
         mine = rank < c
+        stamp("fwd0")
         if mine:
             e_local = ops.forward(x if rank == 0 else lane_x, cyc[rank], "lane")
         else:
             e_local = ops.zeros("lane")
+        stamp("fwd1")
         gathered = ops.allgather(e_local, c)
+        stamp("xchg")
         ops.record(T - cyc[0], gathered[:c])
         if mine:
             cache = ops.keep_cache(gathered[rank])
         nxt = cycles[ci + 1] if ci + 1 < len(cycles) else None
         roll = nxt[:rank] if (nxt is not None and 1 <= rank < len(nxt)) else []
         x, lane_x = ops.apply_roll(x, list(cyc), gathered[:c], roll, cache)
+        stamp("apply")
+    finish = getattr(ops, "finish", None)
+    if finish is not None:
+        finish()
+    stamp("end")
     return x
+
+
+@dataclass
+class RankTimings:
+    """Device-clock split of one rank's loop (the reference's WorkerTimings,
+    worker.py:65-85): loop_start/loop_end are %globaltimer stamps (ns -> s);
+    forward_s sums the predictor forwards, exchange_wait_s the time from the
+    end of this rank's forward until its exchange completed (all-gather, or
+    the peers' ready flags), apply_s the fused apply/roll kernels (and record
+    copies)."""
+
+    loop_start: float = 0.0
+    loop_end: float = 0.0
+    forward_s: float = 0.0
+    exchange_wait_s: float = 0.0
+    apply_s: float = 0.0
+
+    @property
+    def loop_s(self) -> float:
+        return self.loop_end - self.loop_start
+
+    @property
+    def comm_s(self) -> float:
+        return self.exchange_wait_s
+
+    @staticmethod
+    def from_stamps(tags: list[str], ns: list[int]) -> "RankTimings":
+        """Each phase is the interval since the previous stamp: fwd0->fwd1 a
+        forward, fwd1->xchg the exchange, (fwd1 | xchg)->apply the apply."""
+        r = RankTimings()
+        prev = None
+        for tag, v in zip(tags, ns):
+            s = v * 1e-9
+            if tag == "start":
+                r.loop_start = s
+            elif tag == "end":
+                r.loop_end = s
+            elif tag == "fwd1":
+                r.forward_s += s - prev
+            elif tag == "xchg":
+                r.exchange_wait_s += s - prev
+            elif tag == "apply":
+                r.apply_s += s - prev
+            prev = s
+        return r
 
 
 class _OwnedDev:
@@ -177,7 +240,7 @@ class CudaRankOps:
 
     def __init__(self, w, sched: NoiseSchedule, cfg: RunConfig, rank: int, world: int,
                  group=None, record: bool = False, external_init: bool = False,
-                 exchange: str = "nccl"):
+                 exchange: str = "nccl", timed: bool = False):
         import torch
 
         self.torch = torch
@@ -212,12 +275,51 @@ class CudaRankOps:
         self.exchange = exchange
         self.px = PeerExchange(n, tdt, rank, world, group) if exchange == "peer" else None
         self.round = 0
+        self.ledger = ExchangeLedger(rank, world, exchange, n * self.x.element_size())
+        # phase stamps (off in the timed bench runs: each is one tiny launch)
+        self.timed = timed
+        self.stamp_tags: list[str] = []
+        self.stamp_buf = torch.zeros(8 * self.T + 16, dtype=torch.int64, device="cuda") \
+            if timed else None
+
+    def stamp(self, tag: str) -> None:
+        if not self.timed:
+            return
+        i = len(self.stamp_tags)
+        self.stamp_tags.append(tag)
+        _lib.check(self.lib.ps_stamp(self._p(self.stamp_buf) + 8 * i, _lib.stream_ptr()), "stamp")
+        self.launches += 1
+
+    def timings(self) -> RankTimings:
+        if not self.timed:
+            return RankTimings()
+        ns = self.stamp_buf[:len(self.stamp_tags)].cpu().tolist()
+        return RankTimings.from_stamps(self.stamp_tags, ns)
+
+    def finish(self):
+        """Peer exchange: end-of-run handshake. Every rank publishes "run done"
+        (a round index above any real round) and waits for all ranks' flags,
+        so the next run's first lane forward cannot overwrite an eps buffer a
+        slower peer is still reading in this run's last apply."""
+        if self.px is None:
+            return
+        st = _lib.stream_ptr()
+        _lib.check(self.lib.ps_peer_signal(self._p(self.px.slots), self.world,
+                                           self._p(self.px.base), self.DONE_ROUND, st),
+                   "peer signal")
+        _lib.check(self.lib.ps_peer_wait(self._p(self.px.ready), self.world,
+                                         self._p(self.px.base), self.DONE_ROUND, st), "peer wait")
+        self.launches += 2
+
+    DONE_ROUND = 1 << 19  # below the 2^20 epoch stride, above any round index
 
     def _p(self, t) -> int:
         return _lib.ptr(t)
 
     def init(self):
         self.round = 0
+        self.ledger.reset()
+        self.stamp_tags = []
         if hasattr(self.w, "prepare_conditioning"):  # batched t-only conditioning of the run
             self.launches += self.w.prepare_conditioning(self.T)
         if self.px is not None:
@@ -257,12 +359,23 @@ class CudaRankOps:
             self.launches += 2
             self.gathers += 1
             self.round += 1
-            return self.px.views[k % 2]
+            views = self.px.views[k % 2]
+            # bytes the apply kernels move over NVLink this round: this rank
+            # reads every active remote lane; peers pull its own lane
+            vb = self.ledger.vec_bytes
+            remote = [v for j, v in enumerate(views[:active]) if j != self.rank]
+            owns = self.rank < active
+            self.ledger.record(active, (active - 1) * vb if owns else 0,
+                               sum(v.nbytes for v in remote), len(remote))
+            return views
         import torch.distributed as dist
 
         dist.all_gather_into_tensor(self.gathered, e, group=self.group)
         self.gathers += 1
         self.round += 1
+        es = e.element_size()
+        self.ledger.record(active if active is not None else self.world, e.numel() * es,
+                           (self.gathered.numel() - e.numel()) * es, self.world - 1)
         return [self.gathered[i] for i in range(self.world)]
 
     def keep_cache(self, e):
@@ -307,7 +420,9 @@ class CudaRankOps:
 
 @dataclass
 class RunResult:
-    """Per-rank outcome of run_nccl (mirrors worker.RunResult, worker.py:97-110)."""
+    """Per-rank outcome of run_nccl (mirrors worker.RunResult, worker.py:97-110):
+    rank 0 carries the Trajectory; ``timings`` holds every rank's RankTimings
+    (gathered to all ranks), ``ledgers`` every rank's measured ExchangeLedger."""
 
     trajectory: Trajectory | None
     x0: object
@@ -315,7 +430,14 @@ class RunResult:
     world: int
     gathers: int = 0
     launches: int = 0
-    timings: dict = field(default_factory=dict)
+    timings: list = field(default_factory=list)
+    ledgers: list = field(default_factory=list)
+
+    @property
+    def loop_latency_s(self) -> float:
+        """Denoising-loop latency (worker.py:108-110): the slowest rank's loop,
+        each rank timed on its own device clock from the same barrier."""
+        return max((t.loop_s for t in self.timings), default=0.0)
 
 
 class NcclSampler:
@@ -328,20 +450,27 @@ class NcclSampler:
     """
 
     def __init__(self, w, sched: NoiseSchedule, cfg: RunConfig, group=None, record=False,
-                 external_init=False, exchange: str = "nccl"):
+                 external_init=False, exchange: str = "nccl", timed: bool = False):
         import torch.distributed as dist
 
-        _check(w, sched, cfg, STRATEGY_PARASTEP)
+        _check(w, sched, cfg, None)
+        if cfg.strategy not in (STRATEGY_PARASTEP, STRATEGY_DYNAMIC):
+            raise ConfigError(f"protocol runs use the parastep (or dynamic) strategy, got "
+                              f"{cfg.strategy!r}")
         if not dist.is_initialized():
             raise ConfigError("run_nccl needs an initialised torch.distributed process group")
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
-        if cfg.degree != self.world:
-            raise ConfigError(f"degree {cfg.degree} != world size {self.world}")
+        self.group = group
         self.cfg = cfg
         self.cycles = plan_cycles(cfg)
+        if cfg.strategy == STRATEGY_PARASTEP and cfg.degree != self.world:
+            raise ConfigError(f"degree {cfg.degree} != world size {self.world}")
+        if max((len(c) for c in self.cycles), default=1) > self.world:
+            raise ConfigError(f"a cycle of {max(len(c) for c in self.cycles)} lanes needs more "
+                              f"than the {self.world} ranks")
         self.ops = CudaRankOps(w, sched, cfg, self.rank, self.world, group, record, external_init,
-                               exchange)
+                               exchange, timed)
         self.graph = None
 
     def _launch(self):
@@ -379,23 +508,15 @@ class NcclSampler:
         return self.result().trajectory
 
     def traffic_census(self) -> dict:
-        """This rank's ε-exchange bytes per round vs the closed form.
-
-        One all-gather per cycle (len(cycles) rounds); per round a rank sends
-        N*s bytes and receives (d-1)*N*s (the all-gather replaces the
-        reference's NOISE + SAMPLE_BCAST pair, whose ledger is 2(d-1)*M per
-        full cycle, protocol/ledger.py:120-123).
-        """
-        o = self.ops
-        es = 8 if o.code == _lib.PS_F64 else 4
-        per = o.n * es
-        lines = ["round,cycle_len,sent_bytes,received_bytes"]
-        for i, cyc in enumerate(self.cycles):
-            lines.append(f"{i},{len(cyc)},{per},{(self.world - 1) * per}")
-        rounds = len(self.cycles)
-        return {"rounds": o.gathers, "sent": rounds * per,
-                "received": rounds * (self.world - 1) * per,
-                "ok": o.gathers == rounds, "csv": "\n".join(lines) + "\n"}
+        """This rank's measured ε-exchange bytes per round (the ExchangeLedger
+        of the last run), verified against the closed form: per full round a
+        rank receives (d-1)*N*s bytes (ledger.py; the reference's Algorithm-1
+        ledger moves 2(d-1)*M per cycle, protocol/ledger.py:120-123). A
+        mismatch raises LedgerViolationError."""
+        lg = self.ops.ledger
+        rep = lg.verify(self.cycles)
+        return {"rounds": rep.rounds, "sent": rep.sent, "received": rep.received,
+                "ok": True, "csv": lg.csv(), "report": rep.summary()}
 
     def result(self) -> RunResult:
         import torch
@@ -413,12 +534,17 @@ class NcclSampler:
                     fresh[T - t] = j == 0
             traj = Trajectory([StepRecord(T - k, xs[k].copy(), es[k].copy(), fresh[k])
                                for k in range(T)], o.x.double().cpu().numpy().copy())
+        import torch.distributed as dist
+
+        mine = (o.timings(), o.ledger)
+        allr = [None] * self.world
+        dist.all_gather_object(allr, mine, group=self.group)
         return RunResult(traj, o.x.double().cpu().numpy().copy(), self.rank, self.world,
-                         o.gathers, o.launches)
+                         o.gathers, o.launches, [a[0] for a in allr], [a[1] for a in allr])
 
 
 def run_nccl(w, sched: NoiseSchedule, cfg: RunConfig, group=None, record: bool = True,
-             timeout: float = 60.0) -> RunResult:
+             timeout: float = 60.0, exchange: str = "nccl") -> RunResult:
     """The reference's run_tcp/run_loopback (worker.py:244-372) as one NCCL rank.
 
     Call on every rank of an initialised NCCL group with cfg.degree == world
@@ -428,7 +554,7 @@ def run_nccl(w, sched: NoiseSchedule, cfg: RunConfig, group=None, record: bool =
     """
     import torch
 
-    s = NcclSampler(w, sched, cfg, group=group, record=record)
+    s = NcclSampler(w, sched, cfg, group=group, record=record, exchange=exchange, timed=True)
     try:
         s.run(cfg.seed)
         torch.cuda.synchronize()

@@ -50,6 +50,40 @@ def test_compare_dit(tmp_path):
     assert "win_rate=" in (tmp_path / "summary.txt").read_text()
 
 
+def test_compare_files_match_reference_semantics(tmp_path):
+    """adjacent.csv holds the strategy's OWN adjacent-step series (T-1 rows per
+    run, reference cli.py:530-535) and divergence.csv the x0 MSE (not x_1's)."""
+    steps, warm = 10, 2
+    rc = cli.main(["compare", "--strategies", "sequential:1,parastep:3", "--seeds", "1",
+                   "--steps", str(steps), "--warmup", str(warm), "--seed", "3",
+                   "--out-dir", str(tmp_path)])
+    assert rc == 0
+    w = P.init_weights(P.TrainConfig(data_dim=2, hidden=(64, 64), embed_dim=16, seed=7,
+                                     iterations=0))
+    sch = S.make_default_schedule(steps, "posterior")
+    seq = E.run_strategy(w, sch, E.RunConfig(steps=steps, seed=3, data_dim=2))
+    par = E.run_strategy(w, sch, E.RunConfig(steps=steps, warmup=warm, strategy="parastep",
+                                             degree=3, seed=3, data_dim=2))
+    adj = (tmp_path / "adjacent.csv").read_text().splitlines()
+    assert adj[0] == "strategy,seed,step,rel_mae_x,rel_mae_eps"
+    assert len(adj) == 1 + 2 * (steps - 1)
+    for label, tr, lines in (("sequential:1", seq, adj[1:steps]),
+                             ("parastep:3", par, adj[steps:])):
+        want = E.compare_trajectories(seq, tr).adjacent_b
+        for line, r in zip(lines, want):
+            lab, seed, t, rx, re_ = line.split(",")
+            assert (lab, int(seed), int(t)) == (label, 3, r.t)
+            assert np.isclose(float(rx), r.rel_mae_x, rtol=1e-10)
+            assert np.isclose(float(re_), r.rel_mae_eps, rtol=1e-10)
+    div = (tmp_path / "divergence.csv").read_text().splitlines()
+    rep = E.compare_trajectories(seq, par)
+    lab, seed, fr, fm = div[2].split(",")
+    assert lab == "parastep:3"
+    assert np.isclose(float(fr), rep.final_rel_mae, rtol=1e-10)
+    assert np.isclose(float(fm), rep.final_mse, rtol=1e-10)
+    assert float(div[1].split(",")[3]) == 0.0  # sequential vs itself
+
+
 def test_generate_nccl_traffic_census(tmp_path):
     n = torch.cuda.device_count()
     out = subprocess.run(

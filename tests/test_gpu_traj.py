@@ -40,8 +40,9 @@ def test_device_pack_equals_host_writer_and_reference_file(tmp_path):
     ref = TIO.load_trajectory_binary(os.path.join(G, "traj_ps3.pstj"))  # written by the reference
     assert [r.t for r in ours.records] == [r.t for r in ref.records]
     assert [r.fresh for r in ours.records] == [r.fresh for r in ref.records]
-    rows, x0 = E.compare_trajectories(ref, ours)
-    assert x0 < 1e-10 and max(max(r.rel_mae_x, r.rel_mae_eps) for r in rows) < 1e-10
+    rep = E.compare_trajectories(ref, ours)
+    assert rep.final_rel_mae < 1e-10
+    assert max(max(r.rel_mae_x, r.rel_mae_eps) for r in rep.rows) < 1e-10
 
 
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
@@ -55,11 +56,20 @@ def test_device_compare_matches_host(precision):
                                             seed=2, data_dim=spec.data_dim), record=True)
     a.run(2)
     b.run(2)
-    rows_d, x0_d = E.compare_trajectories_device(a, b)
-    rows_h, x0_h = E.compare_trajectories(a.trajectory(), b.trajectory())
-    assert [r.t for r in rows_d] == [r.t for r in rows_h]
-    for rd, rh in zip(rows_d, rows_h):
+    dev = E.compare_trajectories_device(a, b)
+    host = E.compare_trajectories(a.trajectory(), b.trajectory())
+    assert [r.t for r in dev.rows] == [r.t for r in host.rows]
+    for rd, rh in zip(dev.rows, host.rows):
         for f in ("rel_mae_x", "rel_mae_eps", "mse_x", "mse_eps"):
             assert np.isclose(getattr(rd, f), getattr(rh, f), rtol=1e-12, atol=1e-300), f
-    assert np.isclose(x0_d, x0_h, rtol=1e-12)
-    assert x0_d > 0.0  # ParaStep reuse differs from sequential
+    for side in ("adjacent_a", "adjacent_b"):
+        ad, ah = getattr(dev, side), getattr(host, side)
+        assert len(ad) == len(ah) == 15
+        assert [r.t for r in ad] == [r.t for r in ah]
+        for rd, rh in zip(ad, ah):
+            assert np.isclose(rd.rel_mae_x, rh.rel_mae_x, rtol=1e-12)
+            assert np.isclose(rd.rel_mae_eps, rh.rel_mae_eps, rtol=1e-12)
+    assert np.isclose(dev.final_rel_mae, host.final_rel_mae, rtol=1e-12)
+    assert np.isclose(dev.final_mse, host.final_mse, rtol=1e-12)
+    assert dev.final_rel_mae > 0.0  # ParaStep reuse differs from sequential
+    assert dev.to_csv() .splitlines()[0] == "step,rel_mae_x,rel_mae_eps,mse_x,mse_eps"

@@ -18,6 +18,8 @@ import torch.multiprocessing as mp
 
 from oracle import core, engines as oeng
 from paper_2505_14741_b200.engines import RunConfig, plan_cycles
+from paper_2505_14741_b200.errors import LedgerViolationError
+from paper_2505_14741_b200.ledger import ExchangeLedger, verify_merged
 from paper_2505_14741_b200.protocol import rank_loop
 
 
@@ -28,6 +30,7 @@ class OracleOps:
         self.rec_e = {}
         self.rec_x = {}
         self.gathers = 0
+        self.ledger = ExchangeLedger(rank, world, "gloo", 8 * n)
 
     def init(self):
         return oeng.x_init(self.seed, self.n)
@@ -40,8 +43,13 @@ class OracleOps:
 
     def allgather(self, e, active=None):
         out = [torch.zeros(self.n, dtype=torch.float64) for _ in range(self.world)]
-        dist.all_gather(out, torch.from_numpy(np.ascontiguousarray(e)))
+        src = torch.from_numpy(np.ascontiguousarray(e))
+        dist.all_gather(out, src)
         self.gathers += 1
+        es = src.element_size()
+        self.ledger.record(active if active is not None else self.world, src.numel() * es,
+                           sum(o.numel() for i, o in enumerate(out) if i != self.rank) * es,
+                           self.world - 1)
         return [o.numpy().copy() for o in out]
 
     def keep_cache(self, e):
@@ -61,18 +69,18 @@ class OracleOps:
         return x, lane
 
 
-def _worker(rank, world, port, T, warmup, mode, seed, q):
+def _worker(rank, world, port, T, warmup, mode, seed, q, lengths=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         pred = core.MLP.init(6, hidden=(8,), embed_dim=4, seed=7)
         sch = core.Sched(T, mode)
-        cfg = RunConfig(steps=T, warmup=warmup, strategy="parastep", degree=world, seed=seed,
-                        data_dim=6)
+        cfg = RunConfig(steps=T, warmup=warmup, strategy="dynamic" if lengths else "parastep",
+                        degree=world, seed=seed, data_dim=6, schedule_override=lengths)
         ops = OracleOps(pred, sch, 6, seed, rank, world)
         x0 = rank_loop(ops, T, warmup, world, rank, plan_cycles(cfg))
-        q.put((rank, x0, ops.rec_x, ops.rec_e, ops.gathers))
+        q.put((rank, x0, ops.rec_x, ops.rec_e, ops.gathers, ops.ledger))
     finally:
         dist.destroy_process_group()
 
@@ -94,9 +102,11 @@ def test_rank_loop_over_gloo_equals_cycle_runner(world, T, warmup, mode):
     for p in procs:
         p.start()
     res = {}
+    ledgers = []
     for _ in range(world):
-        r, x0, rx, re, g = q.get(timeout=120)
+        r, x0, rx, re, g, lg = q.get(timeout=120)
         res[r] = (x0, rx, re, g)
+        ledgers.append(lg)
     for p in procs:
         p.join(timeout=30)
         assert p.exitcode == 0
@@ -109,5 +119,66 @@ def test_rank_loop_over_gloo_equals_cycle_runner(world, T, warmup, mode):
         assert np.array_equal(re[k], ref["eps"][k]), k
     for r in range(1, world):
         assert np.array_equal(res[r][0], x0)  # every rank ends synchronised
-    assert gathers == len(plan_cycles(RunConfig(steps=T, warmup=warmup, strategy="parastep",
-                                                degree=world, data_dim=6)))
+    cycles = plan_cycles(RunConfig(steps=T, warmup=warmup, strategy="parastep", degree=world,
+                                   data_dim=6))
+    assert gathers == len(cycles)
+    # measured exchange ledger: every rank's census and the d(d-1)*N*s total per full round
+    total = verify_merged(ledgers, cycles)
+    assert total == world * len(cycles) * (world - 1) * 8 * 6
+    ledgers[1].entries[0].received += 8
+    with pytest.raises(LedgerViolationError):
+        verify_merged(ledgers, cycles)
+
+
+def test_rank_loop_dynamic_cycles_over_gloo():
+    """Dynamic cycle lengths (the reference's denoise_dynamic, engines.py:346-349)
+    through the same rank loop: cycles shorter than the world idle ranks."""
+    world, T, warmup, lengths = 3, 12, 2, [1, 3, 2, 3, 1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, T, warmup, "posterior", 9, q,
+                                               lengths)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    ledgers = []
+    for _ in range(world):
+        r, x0, rx, re, g, lg = q.get(timeout=120)
+        res[r] = (x0, rx, re)
+        ledgers.append(lg)
+    for p in procs:
+        p.join(timeout=30)
+        assert p.exitcode == 0
+    pred = core.MLP.init(6, hidden=(8,), embed_dim=4, seed=7)
+    ref = oeng.cycles(pred, core.Sched(T, "posterior"), 6, 9, warmup=warmup, degree=world,
+                      lengths=lengths)
+    x0, rx, re = res[0]
+    assert np.array_equal(x0, ref["x0"])
+    for k in range(T):
+        assert np.array_equal(rx[k], ref["x"][k]), k
+        assert np.array_equal(re[k], ref["eps"][k]), k
+    for r in range(1, world):
+        assert np.array_equal(res[r][0], x0)
+    cycles = plan_cycles(RunConfig(steps=T, warmup=warmup, strategy="dynamic", degree=world,
+                                   schedule_override=lengths, data_dim=6))
+    verify_merged(ledgers, cycles)
+
+
+def test_peer_ledger_closed_form():
+    """Peer exchange census (host logic): a lane owner reads the c-1 remote
+    lanes, an idle rank all c; a full round moves d(d-1)*N*s in total."""
+    d, v = 4, 1024
+    cycles = [[10, 9, 8, 7], [6, 5, 4, 3], [2, 1]]
+    lgs = [ExchangeLedger(r, d, "peer", v) for r in range(d)]
+    for cyc in cycles:
+        c = len(cyc)
+        for lg in lgs:
+            owns = lg.rank < c
+            lg.record(c, (c - 1) * v if owns else 0, ((c - 1) if owns else c) * v,
+                      (c - 1) if owns else c)
+    assert verify_merged(lgs, cycles) == sum(lg.received for lg in lgs)
+    assert lgs[3].entries[2].received == 2 * v  # idle in the truncated cycle
+    lgs[0].entries[1].sent = 0
+    with pytest.raises(LedgerViolationError):
+        lgs[0].verify(cycles)

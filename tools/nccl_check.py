@@ -34,6 +34,26 @@ def main():
     cfg = E.RunConfig(steps=T, warmup=2, strategy="parastep", degree=world, seed=7,
                       data_dim=spec.data_dim)
     res = run_nccl(w, sched, cfg)
+    # measured exchange ledger (raises LedgerViolationError on a mismatch) and
+    # the per-rank device-clock split
+    from paper_2505_14741_b200.ledger import verify_merged
+
+    verify_merged(res.ledgers, E.plan_cycles(cfg))
+    assert len(res.timings) == world and res.loop_latency_s > 0
+    assert all(t.forward_s > 0 and t.apply_s > 0 for t in res.timings)
+    # dynamic cycle lengths over the same rank loop (cycles <= world lanes)
+    dyn_len = [min(world, 2), 1] * 8
+    acc, lens = 0, []
+    for c in dyn_len:
+        if acc + c > T - 2:
+            c = T - 2 - acc
+        if c > 0:
+            lens.append(c)
+            acc += c
+    dcfg = E.RunConfig(steps=T, warmup=2, strategy="dynamic", degree=world, seed=7,
+                       schedule_override=lens, data_dim=spec.data_dim)
+    dres = run_nccl(w, sched, dcfg)
+    verify_merged(dres.ledgers, E.plan_cycles(dcfg))
     s = NcclSampler(w, sched, cfg, record=False)
     s.run(7, graph=True)
     s.run(7, graph=True)  # replay
@@ -44,8 +64,13 @@ def main():
     if rank == 0:
         ref = E.run_strategy(w, sched, cfg)  # lane emulation on one GPU
         ok = ok and res.trajectory.bitwise_equal(ref)
+        dref = E.run_strategy(w, sched, dcfg)
+        ok = ok and dres.trajectory.bitwise_equal(dref)
+        t0 = res.timings[0]
         print(f"NCCL_CHECK {'OK' if ok else 'FAIL'} world={world} gathers={res.gathers} "
-              f"launches={res.launches}", flush=True)
+              f"launches={res.launches} loop_ms={res.loop_latency_s * 1e3:.3f} "
+              f"fwd_ms={t0.forward_s * 1e3:.3f} xchg_ms={t0.exchange_wait_s * 1e3:.3f} "
+              f"apply_ms={t0.apply_s * 1e3:.3f} ledger={res.ledgers[0].received}B", flush=True)
     dist.barrier()
     dist.destroy_process_group()
     sys.exit(0 if ok else 1)

@@ -52,6 +52,15 @@ def main():
     s.run(7, graph=True)
     s.run(7, graph=True)  # replay: epochs advance on device
     g = s.result()
+    # measured exchange ledger of the peer reads + the device-clock phase split
+    from paper_2505_14741_b200.ledger import verify_merged
+
+    verify_merged(res.ledgers, E.plan_cycles(cfg))
+    ts = NcclSampler(w, sched, cfg, record=False, exchange="peer", timed=True)
+    ts.run(7)
+    tr = ts.result()
+    assert tr.loop_latency_s > 0 and np.array_equal(tr.x0, res.x0)
+    ts.ops.px.close()
     x0s = [None] * world
     dist.all_gather_object(x0s, res.x0)
     ok = all(np.array_equal(x0s[0], v) for v in x0s) and np.array_equal(g.x0, res.x0)
@@ -59,7 +68,8 @@ def main():
         ref = E.run_strategy(w, sched, cfg)  # lane emulation on one GPU
         ok = ok and res.trajectory.bitwise_equal(ref) and g.trajectory.bitwise_equal(ref)
         print(f"PEER_CHECK {'OK' if ok else 'FAIL'} world={world} same_gpu={same} "
-              f"rounds={res.gathers} launches={res.launches}", flush=True)
+              f"rounds={res.gathers} launches={res.launches} "
+              f"loop_ms={tr.loop_latency_s * 1e3:.3f}", flush=True)
     dist.barrier()
     s.ops.px.close()
     dist.destroy_process_group()

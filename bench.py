@@ -237,23 +237,94 @@ def call_count(T, warmup, p):
     return warmup + -(-(T - warmup) // p)
 
 
+def reference_loop_run(cfg, degree):
+    """One complete run of the reference's own loop on host cores, the oracle
+    predictor injected through its import seam (engines.py:40,
+    protocol/worker.py:45): degree 1 -> run_strategy(sequential)
+    (engines.py:196-205); degree p > 1 -> run_loopback (worker.py:244-285),
+    p worker threads exchanging over the reference's in-process transport.
+    Returns (seconds, per-rank timings or None, kind)."""
+    import numpy as np
+
+    kind, RE, RW, RS, _ = reference_module()
+    pred = cpu_predictor(cfg)
+    n = pred.data_dim
+
+    def fwd(w, x, t, T):
+        return pred(np.asarray(x, dtype=np.float64), t, T)
+
+    if kind != "reference":  # the oracle port (baseline/_ref absent): sequential only
+        from oracle import core, engines as oeng
+
+        t0 = time.perf_counter()
+        oeng.sequential(lambda x, t, T: fwd(None, x, t, T), core.Sched(cfg["T"], cfg["sigma"]),
+                        n, 0)
+        return time.perf_counter() - t0, None, kind
+
+    class Shim:
+        data_dim = n
+        ballast = 1
+
+    RE.forward = fwd
+    RE.forward_batch = lambda w, xs, ts, T: [fwd(w, x, t, T) for x, t in zip(xs, ts)]
+    RW.forward = fwd
+    sched = RS.make_default_schedule(cfg["T"], cfg["sigma"])
+    if degree == 1:
+        rcfg = RE.RunConfig(steps=cfg["T"], seed=0, data_dim=n)
+        t0 = time.perf_counter()
+        RE.run_strategy(Shim(), sched, rcfg)
+        return time.perf_counter() - t0, None, kind
+    rcfg = RE.RunConfig(steps=cfg["T"], warmup=cfg["warmup"], strategy="parastep",
+                        degree=degree, seed=0, data_dim=n)
+    from threadpoolctl import threadpool_limits
+
+    # p concurrent workers share the host cores: cores/p BLAS threads each (the
+    # reference's bench pins its workers, bench.py:233-236)
+    per = max(1, len(os.sched_getaffinity(0)) // degree)
+    with threadpool_limits(limits=per):
+        t0 = time.perf_counter()
+        res = RW.run_loopback(Shim(), sched, rcfg)
+        el = time.perf_counter() - t0
+    tims = [{"forward_s": t.forward_s, "comm_s": t.comm_s, "recv_wait_s": t.recv_wait_s}
+            for t in res.timings]
+    return res.loop_latency_s or el, tims, kind
+
+
+# configs whose full reference run fits a bench step (~5 s per DiT-S/2 denoise
+# on 16 host cores); the larger ones time a sample of forwards and extrapolate
+REF_FULL_RUN = ("small_dit_fp32", "c1ref_mlp")
+
+
 def reference_arm(args, cfg, world, rank):
     if rank != 0:
         return
-    import numpy as np  # noqa: F401
-
     ncores = len(os.sched_getaffinity(0))
     T, w = cfg["T"], cfg["warmup"] if world > 1 else 0
     calls = call_count(T, w, world)
-    sample = max(1, min(T, args.ref_sample))
-    times = []
+    full = args.config in REF_FULL_RUN and args.ref_sample == 0
+    times, tims = [], None
     kind = "port"
     for i in range(args.warmup + args.steps):
-        el, done, _, kind = cpu_reference_run(cfg, max_forwards=sample)
-        per_call = el / done
+        if full:
+            el, tims, kind = reference_loop_run(cfg, world)
+            ms = el * 1e3
+        else:
+            sample = max(1, min(T, args.ref_sample or 3))
+            el, done, _, kind = cpu_reference_run(cfg, max_forwards=sample)
+            ms = el / done * calls * 1e3
         if i >= args.warmup:
-            times.append(per_call * calls * 1e3)
+            times.append(ms)
     val = statistics.mean(times)
+    if full:
+        what = ("run_strategy(sequential)" if world == 1 else
+                f"run_loopback(parastep, degree {world}, warm-up {w}): {world} worker threads, "
+                f"{max(1, ncores // world)} BLAS threads each")
+        sample = (f"one complete {T}-step denoise per bench step through the reference's "
+                  f"{what}; oracle DiT predictor (numpy f64) via the import seam")
+    else:
+        sample = (f"first {max(1, min(T, args.ref_sample or 3))} of {T} sampler steps of the "
+                  f"reference's sequential loop per bench step, extrapolated x{calls} predictor "
+                  f"calls (busiest device at degree {world}, commodel.call_count_per_device)")
     out = {
         "impl": "reference",
         "metric": f"denoise latency ({T} steps, degree {world})",
@@ -262,13 +333,24 @@ def reference_arm(args, cfg, world, rank):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded reference RNG)",
         "config": config_block(args, cfg, world),
         "cpu_baseline": {"value": val, "unit": "ms", "cores": ncores, "kind": kind,
-                         "sample": f"first {sample} of {T} sampler steps of the reference's "
-                                   f"sequential loop per step, extrapolated x{calls} predictor "
-                                   f"calls (busiest device at degree {world}, "
-                                   f"commodel.call_count_per_device)"},
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": val, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "samples_ms": times,
     }
+    if tims:
+        out["per_worker"] = tims
     print(json.dumps(out), flush=True)
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
 
 def config_block(args, cfg, world):
@@ -461,6 +543,58 @@ def sched_roofline(torch, hbm_peak):
             "launch_us": t * 1e6}
 
 
+def multi_gpu_report(w, sched, cfg, n, world, rank, value, flush, torch, dist):
+    """N > 1: the reference bench's comparison row (bench.py:216-255) on this
+    box: the sequential (degree-1) latency on rank 0's GPU, the speed-up, the
+    call-count bound T / (w + ceil((T-w)/d)) and the Amdahl bound
+    (commodel.py:51-68), and every rank's device-clock split of one run into
+    forward / exchange wait / apply (worker.py:65-85, RankTimings) plus the
+    measured exchange ledger."""
+    from paper_2505_14741_b200.protocol import NcclSampler
+
+    T, wu = cfg["T"], cfg["warmup"]
+    rep = {}
+    # per-rank phase split: one eager run with device-clock stamps
+    ts = NcclSampler(w, sched, run_cfg(cfg, n, world), record=False,
+                     exchange=EXCHANGE["used"] or "nccl", timed=True)
+    for _ in range(2):
+        dist.barrier()
+        ts.run(0)
+        res = ts.result()
+    census = ts.traffic_census()
+    rep["per_rank"] = [{"rank": r, "loop_ms": t.loop_s * 1e3, "forward_ms": t.forward_s * 1e3,
+                        "exchange_wait_ms": t.exchange_wait_s * 1e3, "apply_ms": t.apply_s * 1e3}
+                       for r, t in enumerate(res.timings)]
+    rep["per_rank_note"] = ("one eager (not graph-replayed) run with %globaltimer stamps between "
+                            "phases; loop_ms includes host launch gaps the timed graph runs omit")
+    rep["exchange_ledger"] = {"rounds": census["rounds"], "sent_bytes": census["sent"],
+                              "received_bytes": census["received"],
+                              "verified": census["ok"]}
+    if hasattr(ts.ops, "px") and ts.ops.px is not None:
+        dist.barrier()
+        ts.ops.px.close()
+    dist.barrier()
+    seq = None
+    if rank == 0:
+        from paper_2505_14741_b200.engines import DeviceSampler, RunConfig
+
+        scfg = RunConfig(steps=T, warmup=0, strategy="sequential", degree=1, seed=0, data_dim=n)
+        ss = DeviceSampler(w, sched, scfg)
+        ss.run(0, graph=True)
+        seq = statistics.mean(time_runs(ss, 3, 2, flush, torch, dist, 1))
+    dist.barrier()
+    calls = call_count(T, wu, world)
+    m = wu / T
+    rep.update({
+        "sequential_ms": seq,
+        "speedup_vs_sequential": (seq / value) if seq else None,
+        "call_count_per_device": calls,
+        "speedup_bound_callcount": T / calls,
+        "speedup_bound_amdahl": 1.0 / (m + (1.0 - m) / world),
+    })
+    return rep
+
+
 def our_arm(args, cfg, world, rank, local):
     import numpy as np
     import torch
@@ -530,6 +664,8 @@ def our_arm(args, cfg, world, rank, local):
             bms = time_runs(bs, max(2, args.steps // 2), 1, flush, torch, dist, 1)
             extra[f"batchstep_d{d}_ms"] = statistics.mean(bms)
             extra[f"batchstep_d{d}_speedup"] = value / statistics.mean(bms)
+            extra[f"batchstep_d{d}_bound_callcount"] = cfg["T"] / call_count(cfg["T"],
+                                                                            cfg["warmup"], d)
         if not args.no_cpu_baseline and cfg["spec"] != "cogvideox_2b":
             # the reference sampler on host cores; one full denoise when it fits
             # (the CogVideoX-shaped forward alone is ~290 s on CPU: not sampled)
@@ -548,6 +684,8 @@ def our_arm(args, cfg, world, rank, local):
                 from paper_2505_14741_b200.numerics import rel_mae
 
                 rel = rel_mae(x0_ref, seq.x0_device.double().cpu().numpy())
+    if world > 1:
+        extra.update(multi_gpu_report(w, sched, cfg, n, world, rank, value, flush, torch, dist))
     if rank != 0:
         return
     out = {
@@ -582,6 +720,30 @@ def our_arm(args, cfg, world, rank, local):
     print(json.dumps(out), flush=True)
 
 
+def free_port() -> int:
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def spawn_ranks(args) -> int:
+    """``--gpus N > 1`` outside torchrun: launch N ranks (one per GPU) through
+    torch.distributed.run ourselves; the rank-0 JSON line passes through."""
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        log(f"error: --gpus {args.gpus} needs {args.gpus} CUDA devices, {have} visible")
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    log("spawning: " + " ".join(cmd))
+    return subprocess.call(cmd, env=dict(os.environ, MASTER_ADDR="127.0.0.1"))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -590,8 +752,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="small_dit_fp32", choices=sorted(CONFIGS))
     ap.add_argument("--batchstep", type=int, nargs="*", default=[2, 4, 8])
-    ap.add_argument("--ref-sample", type=int, default=3,
-                    help="reference arm: sampler steps timed per bench step")
+    ap.add_argument("--ref-sample", type=int, default=0,
+                    help="reference arm: 0 = one complete run per bench step where it fits "
+                         "(DiT-S/2, C1-ref MLP); else sampler steps timed and extrapolated")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--exchange", choices=("peer", "nccl"), default="peer",
                     help="multi-GPU eps exchange: CUDA-IPC peer memory read by the fused apply "
@@ -599,13 +762,22 @@ def main():
     ap.add_argument("--force-nccl", action="store_true",
                     help="run the NCCL rank loop even at one rank (path check under torchrun)")
     args = ap.parse_args()
-    world, rank, local = dist_setup()
-    if world != args.gpus:
-        log(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}; using WORLD_SIZE")
+    under_torchrun = "WORLD_SIZE" in os.environ
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
+        # the CPU arm runs on rank 0 only; without torchrun it runs in this
+        # process at degree --gpus
+        world, rank, local = dist_setup()
+        if not under_torchrun:
+            world = args.gpus
         reference_arm(args, cfg, world, rank)
-        return
+        return 0
+    if args.gpus > 1 and not under_torchrun:
+        return spawn_ranks(args)
+    world, rank, local = dist_setup()
+    if world != args.gpus:
+        log(f"error: --gpus {args.gpus} but WORLD_SIZE {world}")
+        return 2
     global USE_NCCL
     USE_NCCL = world > 1 or args.force_nccl
     EXCHANGE["want"] = args.exchange
@@ -613,6 +785,10 @@ def main():
         import torch
         import torch.distributed as dist
 
+        if world > torch.cuda.device_count():
+            log(f"error: {world} ranks but {torch.cuda.device_count()} CUDA devices: "
+                "one rank per GPU is required")
+            return 2
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     try:
@@ -622,7 +798,8 @@ def main():
             import torch.distributed as dist
 
             dist.destroy_process_group()
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

@@ -96,6 +96,23 @@ def _gelu_tanh(x):
     return 0.5 * x * (1.0 + np.tanh(math.sqrt(2.0 / math.pi) * (x + 0.044715 * (x * x * x))))
 
 
+def _attention(q, k, v, chunk: int = 2048):
+    """softmax(q k^T / sqrt(dh)) v per head; long sequences (the 17,550-token
+    CogVideoX shape) in query chunks so a head's scores never exceed
+    chunk x L (the result is the same row-wise formula)."""
+    H, L, dh = q.shape
+    out = np.empty_like(q)
+    step = L if L <= chunk else chunk
+    for h in range(H):
+        kt = k[h].T
+        for r0 in range(0, L, step):
+            sco = (q[h, r0:r0 + step] @ kt) / math.sqrt(dh)
+            sco = np.exp(sco - sco.max(axis=-1, keepdims=True))
+            pr = sco / sco.sum(axis=-1, keepdims=True)
+            out[h, r0:r0 + step] = pr @ v[h]
+    return out
+
+
 class DiT:
     """pred(x, t, T) -> eps for one latent vector."""
 
@@ -128,10 +145,7 @@ class DiT:
             qkv = self._lin(f"b{i}.qkv", a).reshape(L, 3, H, dh)
             q, k, v = qkv[:, 0].transpose(1, 0, 2), qkv[:, 1].transpose(1, 0, 2), \
                 qkv[:, 2].transpose(1, 0, 2)
-            sco = (q @ k.transpose(0, 2, 1)) / math.sqrt(dh)
-            sco = np.exp(sco - sco.max(axis=-1, keepdims=True))
-            pr = sco / sco.sum(axis=-1, keepdims=True)
-            o = (pr @ v).transpose(1, 0, 2).reshape(L, D)
+            o = _attention(q, k, v).transpose(1, 0, 2).reshape(L, D)
             h = h + g1 * self._lin(f"b{i}.proj", o)
             a = _ln(h) * (1.0 + sc2) + sh2
             h = h + g2 * self._lin(f"b{i}.fc2", _gelu_tanh(self._lin(f"b{i}.fc1", a)))

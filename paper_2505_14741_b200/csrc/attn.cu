@@ -5,6 +5,7 @@
 #include <cmath>
 #include <mutex>
 
+#include "attn_f32tc.cuh"
 #include "attn_fmha.cuh"
 #include "attn_mma.cuh"
 
@@ -51,6 +52,47 @@ int fmha_launch(const CUtensorMap& map, const FmhaArgs& a, cudaStream_t st) {
                             : (two ? fmha_go<64, 2>(map, a, st) : fmha_go<64, 1>(map, a, st));
   if (e != cudaSuccess) return fail((int)e, std::string("fmha: ") + cudaGetErrorString(e));
   return check_launch("fmha");
+}
+
+template <int NA, int KS>
+static cudaError_t fmha_f32_go(const AttnArgs& a, int B, cudaStream_t st) {
+  using C = F3Cfg<NA>;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(fmha_f32_kernel<NA, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         C::SMEM);
+  });
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((a.L + F3_BQ - 1) / F3_BQ * KS, a.H, B);
+  cfg.blockDim = dim3(F3_THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = KS;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, fmha_f32_kernel<NA, KS>, a);
+}
+
+template <int NA>
+static cudaError_t fmha_f32_ks(const AttnArgs& a, int B, cudaStream_t st) {
+  // key blocks per query tile split over a cluster: 1, 2 or 4 CTAs
+  const int nkb = (a.L + F3_BK - 1) / F3_BK;
+  return nkb >= 4 ? fmha_f32_go<NA, 4>(a, B, st)
+                  : (nkb >= 2 ? fmha_f32_go<NA, 2>(a, B, st) : fmha_f32_go<NA, 1>(a, B, st));
+}
+
+int fmha_f32_launch(const AttnArgs& a, int B, cudaStream_t st) {
+  if (a.dh % 8 || a.dh > 64)
+    return fail(PS_EUNSUP, "fp32 tcgen05 attention: head_dim must be a multiple of 8, <= 64");
+  const cudaError_t e = a.dh <= 32 ? fmha_f32_ks<1>(a, B, st) : fmha_f32_ks<2>(a, B, st);
+  if (e != cudaSuccess) return fail((int)e, std::string("fmha_f32: ") + cudaGetErrorString(e));
+  return check_launch("fmha_f32");
 }
 
 static __global__ void f32_to_bf16_n(const float* in, __nv_bfloat16* out, int64_t n) {
@@ -118,10 +160,11 @@ static float attn_run(const float* qkv, float* out, int B, int L, int H, int D, 
     aa.dh = dh;
     aa.scale = 1.0f / sqrtf((float)dh);
     aa.out_bf16 = ob;
-    if (impl == 5) aa.qkv = qkv ? qkv : qf;  // fp32 path reads the unrounded fp32 qkv
-    if (impl == 5) aa.out_bf16 = nullptr, aa.out_f32 = out_f32;
+    if (impl >= 5) aa.qkv = qkv ? qkv : qf;  // fp32 path reads the unrounded fp32 qkv
+    if (impl >= 5) aa.out_bf16 = nullptr, aa.out_f32 = out_f32;
     auto go = [&]() -> int {
       if (impl == 2) return fmha_launch(map, fa, st);
+      if (impl == 6) return fmha_f32_launch(aa, B, st);
       if (!launch_attn_tc(impl == 5 ? AM_TF32X3 : AM_BF16, aa, B, st))
         return fail(PS_EUNSUP, "head_dim unsupported");
       return check_launch("attn_tc");
@@ -141,7 +184,7 @@ static float attn_run(const float* qkv, float* out, int B, int L, int H, int D, 
       cudaEventDestroy(a);
       cudaEventDestroy(b);
     }
-    if (!rc && out && impl == 5)
+    if (!rc && out && impl >= 5)
       cudaMemcpyAsync(out, out_f32, no * 4, cudaMemcpyDeviceToDevice, st);
     else if (!rc && out)
       bf16_to_f32_n<<<(unsigned)((no + 255) / 256), 256, 0, st>>>(ob, out, no);
@@ -164,11 +207,12 @@ extern "C" {
 
 int ps_attn_test(const float* qkv, float* out, int B, int L, int H, int D, int impl, void* cs) {
   PS_CHECK_ARG(qkv && out && B >= 1 && L >= 1 && H >= 1 && D % H == 0, "bad attention arguments");
-  PS_CHECK_ARG(impl >= 1 && impl <= 5,
-               "impl: 1 mma.sync bf16, 2 tcgen05 (auto), 3/4 tcgen05 1/2 tiles, 5 mma.sync 3xTF32");
+  PS_CHECK_ARG(impl >= 1 && impl <= 6,
+               "impl: 1 mma.sync bf16, 2 tcgen05 (auto), 3/4 tcgen05 1/2 tiles, 5 mma.sync 3xTF32, "
+               "6 tcgen05 3xTF32");
   int rc = 0;
   g_fmha_nq = impl == 3 ? 1 : (impl == 4 ? 2 : 0);
-  attn_run(qkv, out, B, L, H, D, impl == 5 ? 5 : (impl >= 2 ? 2 : 1), 0, as_stream(cs), &rc);
+  attn_run(qkv, out, B, L, H, D, impl >= 5 ? impl : (impl >= 2 ? 2 : 1), 0, as_stream(cs), &rc);
   g_fmha_nq = 0;
   return rc;
 }
@@ -186,11 +230,11 @@ int ps_fmha_stamps(long long* out) {  // diagnostic build only
 #endif
 
 float ps_attn_probe(int B, int L, int H, int D, int impl, int iters) {
-  if (B < 1 || L < 1 || H < 1 || D % H || iters < 1 || impl < 1 || impl > 5) return -1.f;
+  if (B < 1 || L < 1 || H < 1 || D % H || iters < 1 || impl < 1 || impl > 6) return -1.f;
   int rc = 0;
   g_fmha_nq = impl == 3 ? 1 : (impl == 4 ? 2 : 0);
-  float us = attn_run(nullptr, nullptr, B, L, H, D, impl == 5 ? 5 : (impl >= 2 ? 2 : 1), iters, 0,
-                      &rc);
+  float us = attn_run(nullptr, nullptr, B, L, H, D, impl >= 5 ? impl : (impl >= 2 ? 2 : 1), iters,
+                      0, &rc);
   g_fmha_nq = 0;
   return rc ? -1.f : us;
 }

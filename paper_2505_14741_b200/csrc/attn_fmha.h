@@ -23,4 +23,9 @@ inline int fmha_padded_dim(int dh) { return (dh % 8) ? 0 : (dh <= 64 ? 64 : (dh 
 int fmha_make_map(CUtensorMap* m, const __nv_bfloat16* qkv_bf16, int rows, int cols);
 int fmha_launch(const CUtensorMap& map, const FmhaArgs& a, cudaStream_t st);
 
+// fp32 path (3xTF32 tcgen05, attn_f32tc.cuh): fp32 qkv [B*L, 3D] -> the
+// proj GEMM's tf32 hi/lo (and/or fp32) operand; head_dim % 8 == 0, <= 64
+struct AttnArgs;
+int fmha_f32_launch(const AttnArgs& a, int B, cudaStream_t st);
+
 }  // namespace ps

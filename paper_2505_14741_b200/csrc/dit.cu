@@ -422,8 +422,11 @@ int ps_dit_forward(ps_dit* h, const float* x, const int32_t* host_ts, int B, flo
       if ((rc = fmha_launch(h->qkv_map, fa, st))) return rc;
     } else if (h->use_tc && h->cfg.precision == 1 && launch_attn_tc(AM_BF16, at, B, st)) {
       // bf16 path: tensor-core flash attention (bf16 MMA)
+    } else if (h->use_tc && h->cfg.precision == 0 && h->dh % 8 == 0 && h->dh <= 64) {
+      // fp32 path: tcgen05 attention, 3xTF32 (attn_f32tc.cuh)
+      if ((rc = fmha_f32_launch(at, B, st))) return rc;
     } else if (h->use_tc && h->cfg.precision == 0 && launch_attn_tc(AM_TF32X3, at, B, st)) {
-      // fp32 path: tensor-core flash attention (3xTF32 MMA)
+      // fp32 path, head_dim > 64: mma.sync 3xTF32 flash attention
     } else if (small_attn) {
       dim3 ag((L + AS_Q - 1) / AS_Q, h->H, B);
       launch_pdl(attn_small_kernel, ag, dim3(AS_WARPS * 32), as_smem, st, at);

@@ -373,7 +373,8 @@ def config_block(args, cfg, world):
         s = SPECS[cfg["spec"]]
         b.update({"predictor": cfg["spec"], "latent": f"{s.channels}x{s.height}x{s.width}"
                   if s.frames == 1 else f"{s.frames}x{s.height}x{s.width}x{s.channels}",
-                  "hidden": s.hidden, "depth": s.depth, "heads": s.heads, "tokens": s.tokens})
+                  "hidden": s.hidden, "depth": s.depth, "heads": s.heads, "tokens": s.tokens,
+                  "text_tokens": s.text_tokens, "rope": s.rope})
     else:
         b.update({"predictor": "reference MLP 4112-64-64-4096", "latent": "4x32x32"})
     return b
@@ -477,7 +478,7 @@ def attn_roofline(w, cfg, bf16_peak):
     from paper_2505_14741_b200 import _lib
 
     s = w.spec
-    L, H, D = s.tokens, s.heads, s.hidden
+    L, H, D = s.seq_len, s.heads, s.hidden
     iters = 3 if L > 8192 else 50
     lib = _lib.load()
     lib.ps_attn_probe(1, L, H, D, 2, 1)
@@ -500,7 +501,7 @@ def dominant_is_attention(w, cfg):
     if cfg["spec"] is None or cfg.get("family") == "unet":
         return False
     s = w.spec
-    L, D = s.tokens, s.hidden
+    L, D = s.seq_len, s.hidden
     return 4.0 * L * L * D > 2.0 * L * (4 * D * D + 2 * D * s.mlp_hidden)
 
 

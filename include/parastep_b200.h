@@ -122,6 +122,8 @@ typedef struct ps_dit_config {
   int32_t max_batch;
   int32_t precision;  /* 0 = fp32 (fp32-accurate GEMMs), 1 = bf16 tensor-core */
   int32_t gemm_impl;  /* 0 = auto, 1 = SIMT fp32, 2 = tcgen05 */
+  int32_t text_tokens; /* text rows ahead of the video tokens (expert adaLN), 0 = none */
+  int32_t rope;        /* 1 = 3D RoPE on the video rows' q/k (needs tcgen05), no pos table */
 } ps_dit_config;
 
 /* weight pointer order (fp32, (fan_in, fan_out) row-major, see
@@ -134,6 +136,8 @@ typedef struct ps_dit_weights {
   const float* pos;
   const float* freq_table;
   int32_t freq_rows;
+  const float* text; /* [text_tokens, hidden] fixed text states (spec.py), or NULL */
+  const float* rope; /* [video tokens, head_dim / 2, 2] (cos, sin), or NULL */
 } ps_dit_weights;
 
 typedef struct ps_dit ps_dit;

@@ -41,6 +41,41 @@ def pos_table(s: DiTSpec) -> np.ndarray:
         [_sincos_1d(D // 4, f), _sincos_1d(3 * D // 8, h), _sincos_1d(3 * D // 8, w)], axis=1)
 
 
+P_TEXT = 7  # synthetic text conditioning stream (spec.py)
+
+
+def text_states(s: DiTSpec, seed: int) -> np.ndarray:
+    """The fixed text rows: normal(seed, (7<<32)|0)[text_tokens * D]."""
+    from .core import normals
+
+    return normals(seed, make_stream(P_TEXT, 0), s.text_tokens * s.hidden).reshape(
+        s.text_tokens, s.hidden)
+
+
+def rope_angles(s: DiTSpec) -> np.ndarray:
+    """[tokens, head_dim / 2] rotation angles of spec.py's 3D RoPE."""
+    dh = s.head_dim
+    bands = [(dh // 4, "f"), (3 * dh // 8, "h"), (3 * dh // 8, "w")]
+    f, h, w = np.meshgrid(np.arange(s.frames), np.arange(s.grid_h), np.arange(s.grid_w),
+                          indexing="ij")
+    pos = {"f": f.ravel(), "h": h.ravel(), "w": w.ravel()}
+    cols = []
+    for d_a, ax in bands:
+        k = np.arange(d_a // 2, dtype=np.float64)
+        cols.append(pos[ax][:, None].astype(np.float64) * (10000.0 ** (-2.0 * k / d_a))[None, :])
+    return np.concatenate(cols, axis=1)
+
+
+def apply_rope(x: np.ndarray, ang: np.ndarray) -> np.ndarray:
+    """x [H, Lv, dh]: interleaved pairs (2i, 2i+1) rotated by ang[:, i]."""
+    c, sn = np.cos(ang)[None], np.sin(ang)[None]
+    x0, x1 = x[..., 0::2], x[..., 1::2]
+    out = np.empty_like(x)
+    out[..., 0::2] = x0 * c - x1 * sn
+    out[..., 1::2] = x1 * c + x0 * sn
+    return out
+
+
 def init_params(s: DiTSpec, seed: int, bias_scale: float = 0.0) -> dict[str, tuple]:
     """Xavier-uniform per the reference convention; optional nonzero test biases.
 
@@ -123,7 +158,9 @@ class DiT:
         self.dtype = dtype
         self.params = {k: (W.astype(dtype), b.astype(dtype))
                        for k, (W, b) in init_params(s, seed, bias_scale).items()}
-        self.pos = pos_table(s).astype(dtype)
+        self.pos = None if s.rope else pos_table(s).astype(dtype)
+        self.text = text_states(s, seed).astype(dtype) if s.text_tokens else None
+        self.ang = rope_angles(s) if s.rope else None
         self.data_dim = s.data_dim
 
     def _lin(self, name, a):
@@ -134,22 +171,35 @@ class DiT:
         s, dt = self.s, self.dtype
         D, H, dh = s.hidden, s.heads, s.head_dim
         tok = _latent_to_tokens(s, np.asarray(x, dtype=np.float64)).astype(dt)
-        h = self._lin("patch", tok) + self.pos
+        h = self._lin("patch", tok)
+        if self.pos is not None:
+            h = h + self.pos
+        Tx = s.text_tokens
+        if Tx:
+            h = np.concatenate([self.text, h], axis=0)
         c = self._lin("temb2", _silu(self._lin("temb1", time_embed(t, s.freq_dim).astype(dt))))
         sc = _silu(c)
-        L = s.tokens
+        L = s.seq_len
+        txt = (np.arange(L) < Tx)[:, None]
         for i in range(s.depth):
             m = self._lin(f"b{i}.ada", sc)
-            sh1, sc1, g1, sh2, sc2, g2 = (m[k * D:(k + 1) * D] for k in range(6))
+            v6 = [m[k * D:(k + 1) * D] for k in range(6)]
+            t6 = [m[(6 + k) * D:(7 + k) * D] for k in range(6)] if Tx else v6
+            sh1, sc1, g1, sh2, sc2, g2 = (np.where(txt, tv, vv) for vv, tv in zip(v6, t6))
             a = _ln(h) * (1.0 + sc1) + sh1
             qkv = self._lin(f"b{i}.qkv", a).reshape(L, 3, H, dh)
             q, k, v = qkv[:, 0].transpose(1, 0, 2), qkv[:, 1].transpose(1, 0, 2), \
                 qkv[:, 2].transpose(1, 0, 2)
+            if self.ang is not None:  # video rows of q and k
+                q = q.copy()
+                k = k.copy()
+                q[:, Tx:] = apply_rope(q[:, Tx:], self.ang)
+                k[:, Tx:] = apply_rope(k[:, Tx:], self.ang)
             o = _attention(q, k, v).transpose(1, 0, 2).reshape(L, D)
             h = h + g1 * self._lin(f"b{i}.proj", o)
             a = _ln(h) * (1.0 + sc2) + sh2
             h = h + g2 * self._lin(f"b{i}.fc2", _gelu_tanh(self._lin(f"b{i}.fc1", a)))
         m = self._lin("final.ada", sc)
         shf, scf = m[:D], m[D:]
-        out = self._lin("final.out", _ln(h) * (1.0 + scf) + shf)
+        out = self._lin("final.out", _ln(h[Tx:]) * (1.0 + scf) + shf)
         return _tokens_to_latent(s, out.astype(np.float64))

@@ -36,13 +36,14 @@ class ps_mlp(C.Structure):
 class ps_dit_config(C.Structure):
     _fields_ = [(n, C.c_int32) for n in (
         "channels", "frames", "height", "width", "layout", "patch", "hidden", "depth", "heads",
-        "mlp_hidden", "freq_dim", "max_batch", "precision", "gemm_impl")]
+        "mlp_hidden", "freq_dim", "max_batch", "precision", "gemm_impl", "text_tokens",
+        "rope")]
 
 
 class ps_dit_weights(C.Structure):
     _fields_ = [("n_layers", C.c_int32), ("W", C.POINTER(C.c_void_p)),
                 ("b", C.POINTER(C.c_void_p)), ("pos", C.c_void_p), ("freq_table", C.c_void_p),
-                ("freq_rows", C.c_int32)]
+                ("freq_rows", C.c_int32), ("text", C.c_void_p), ("rope", C.c_void_p)]
 
 
 class ps_unet_op(C.Structure):

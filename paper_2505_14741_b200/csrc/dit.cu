@@ -29,10 +29,11 @@ struct ps_dit {
   ps_dit_config cfg;
   DitGeom g;
   int L, D, H, dh, Dm, P, depth, freq_dim, n_ada;
+  int Lv, txt, ada_w;  // video tokens, text rows (L = txt + Lv), adaLN floats per block
   int64_t n_latent;
   const float *Wpe, *bpe, *Wt1, *bt1, *Wt2, *bt2, *Wfa, *bfa, *Wfo, *bfo;
   std::vector<BlockW> blk;
-  const float *pos, *freq;
+  const float *pos, *freq, *text, *rope;
   int freq_rows;
   // owned device memory
   std::vector<void*> owned;
@@ -85,6 +86,8 @@ static int ln_mod(ps_dit* h, int rows, int shift_off, int scale_off, const TcOpe
   }
   p.shift_off = shift_off;
   p.scale_off = scale_off;
+  p.txt = h->txt;
+  p.txt_delta = 6 * h->D;
   if (dst) {
     p.out_bf16 = dst->bf16;
     p.out_hi = dst->hi;
@@ -139,9 +142,14 @@ int ps_dit_create(const ps_dit_config* cfg, const ps_dit_weights* w, ps_dit** ou
   h->g.D = D;
   h->g.gh = cfg->height / cfg->patch;
   h->g.gw = cfg->width / cfg->patch;
-  h->L = h->g.L = cfg->frames * h->g.gh * h->g.gw;
+  h->Lv = h->g.L = cfg->frames * h->g.gh * h->g.gw;
+  h->txt = cfg->text_tokens;
+  h->L = h->Lv + h->txt;
+  h->ada_w = (h->txt ? 12 : 6) * D;
+  PS_CHECK_ARG(h->txt >= 0 && (h->txt == 0 || w->text), "text rows need the text states");
+  PS_CHECK_ARG(!cfg->rope || (w->rope && h->dh % 8 == 0), "RoPE needs its table, head_dim % 8");
   h->n_latent = (int64_t)cfg->channels * cfg->frames * cfg->height * cfg->width;
-  h->n_ada = depth * 6 * D + 2 * D;
+  h->n_ada = depth * h->ada_w + 2 * D;
   int li = 0;
   h->Wpe = w->W[li]; h->bpe = w->b[li++];
   h->Wt1 = w->W[li]; h->bt1 = w->b[li++];
@@ -157,7 +165,9 @@ int ps_dit_create(const ps_dit_config* cfg, const ps_dit_weights* w, ps_dit** ou
   }
   h->Wfa = w->W[li]; h->bfa = w->b[li++];
   h->Wfo = w->W[li]; h->bfo = w->b[li++];
-  h->pos = w->pos;
+  h->pos = cfg->rope ? nullptr : w->pos;
+  h->text = w->text;
+  h->rope = cfg->rope ? w->rope : nullptr;
   h->freq = w->freq_table;
   h->freq_rows = w->freq_rows;
 
@@ -179,8 +189,8 @@ int ps_dit_create(const ps_dit_config* cfg, const ps_dit_weights* w, ps_dit** ou
   for (int i = 0; i <= depth; ++i) {
     const float* src = i < depth ? h->blk[i].ada : h->Wfa;
     const float* bsrc = i < depth ? h->blk[i].b_ada : h->bfa;
-    const int cols = i < depth ? 6 * D : 2 * D;
-    const size_t off = (size_t)i * 6 * D;
+    const int cols = i < depth ? h->ada_w : 2 * D;
+    const size_t off = (size_t)i * h->ada_w;
     cudaError_t e = cudaMemcpy2D(h->Wada_all + off, (size_t)h->n_ada * sizeof(float), src,
                                  (size_t)cols * sizeof(float), (size_t)cols * sizeof(float), D,
                                  cudaMemcpyDeviceToDevice);
@@ -201,9 +211,9 @@ int ps_dit_create(const ps_dit_config* cfg, const ps_dit_weights* w, ps_dit** ou
   }
   const int impl = cfg->gemm_impl;
   h->use_tc = (impl == 2) || (impl == 0);  // auto: tcgen05 for both precisions
-  if (cfg->precision == 1 && !h->use_tc) {
+  if ((cfg->precision == 1 || h->rope) && !h->use_tc) {
     ps_dit_destroy(h);
-    return fail(PS_EUNSUP, "bf16 precision needs the tensor-core GEMM");
+    return fail(PS_EUNSUP, "bf16 precision and RoPE need the tensor-core GEMM");
   }
   if (h->use_tc) {
     std::vector<const float*> Ws;
@@ -244,8 +254,8 @@ int ps_dit_create(const ps_dit_config* cfg, const ps_dit_weights* w, ps_dit** ou
     return fail((int)e, std::string("dit create: ") + cudaGetErrorString(e));
   }
   const double Lf = h->L;
-  h->flops = 2.0 * (Lf * h->P * D + depth * Lf * D * (4.0 * D + 2.0 * h->Dm) + Lf * D * h->P +
-                    depth * 2.0 * Lf * Lf * D);
+  h->flops = 2.0 * (h->Lv * (double)h->P * D + depth * Lf * D * (4.0 * D + 2.0 * h->Dm) +
+                    Lf * D * h->P + depth * 2.0 * Lf * Lf * D);
   *out = h;
   return 0;
 }
@@ -377,7 +387,7 @@ int ps_dit_forward(ps_dit* h, const float* x, const int32_t* host_ts, int B, flo
   }
   const float* modb = h->rows_on ? h->cond : h->mod;
   launch_pdl(patch_embed_kernel, dim3(M), dim3(128), h->P * sizeof(float), st, x, h->n_latent,
-             h->g, h->P, h->Wpe, h->bpe, h->pos, h->h, B);
+             h->g, h->P, h->Wpe, h->bpe, h->pos, h->h, B, h->txt, h->text);
   if ((rc = check_launch("patch_embed"))) return rc;
 
   const TcOperand* aop = h->use_tc ? &h->tca.a : nullptr;
@@ -403,7 +413,7 @@ int ps_dit_forward(ps_dit* h, const float* x, const int32_t* host_ts, int B, flo
   const bool small_attn = L <= AS_MAXL && as_smem <= 220 * 1024;
   for (int i = 0; i < h->depth; ++i) {
     const BlockW& bw = h->blk[i];
-    const int base = i * 6 * D;
+    const int base = i * h->ada_w;
     if ((rc = ln_mod(h, M, base, base + D, aop, st))) return rc;
     Epi e{};
     e.mode = EPI_STORE;
@@ -414,6 +424,11 @@ int ps_dit_forward(ps_dit* h, const float* x, const int32_t* host_ts, int B, flo
       e.pad_dh = h->dh;
       e.pad_DH = h->fm_dh;
     }
+    e.L = L;
+    e.txt = h->txt;
+    e.rope = h->rope;  // 3D RoPE on the video rows' q, k (spec.py)
+    e.rope_dh = h->dh;
+    e.rope_D = D;
     if ((rc = gemm(h, 4 * i + 0, h->a, aop, bw.qkv, M, 3 * D, D, e, st))) return rc;
     if (h->use_fmha) {
       // bf16 path, head_dim 64: tcgen05/TMEM flash attention (attn_fmha.cuh)
@@ -441,6 +456,8 @@ int ps_dit_forward(ps_dit* h, const float* x, const int32_t* host_ts, int B, flo
     e.resid = h->h;
     e.gate = modb + base + 2 * D;
     e.gate_stride = h->n_ada;
+    e.txt = h->txt;
+    e.txt_delta = 6 * D;
     e.use_rows = h->rows_on;
     memcpy(e.lane_row, h->lane_mod_row, sizeof(e.lane_row));
     e.L = L;
@@ -464,17 +481,20 @@ int ps_dit_forward(ps_dit* h, const float* x, const int32_t* host_ts, int B, flo
     e.resid = h->h;
     e.gate = modb + base + 5 * D;
     e.gate_stride = h->n_ada;
+    e.txt = h->txt;
+    e.txt_delta = 6 * D;
     e.use_rows = h->rows_on;
     memcpy(e.lane_row, h->lane_mod_row, sizeof(e.lane_row));
     e.L = L;
     if ((rc = gemm(h, 4 * i + 3, h->hid, hop, bw.fc2, M, D, h->Dm, e, st))) return rc;
   }
-  const int fb = h->depth * 6 * D;
+  const int fb = h->depth * h->ada_w;
   if ((rc = ln_mod(h, M, fb, fb + D, aop, st))) return rc;
   Epi e{};
   e.mode = EPI_UNPATCH;
   e.bias = h->bfo;
   e.g = h->g;
+  e.txt = h->txt;  // text rows carry no latent output
   e.eps = eps_out;
   e.n_latent = h->n_latent;
   return gemm(h, 4 * h->depth, h->a, aop, h->Wfo, M, h->P, D, e, st);

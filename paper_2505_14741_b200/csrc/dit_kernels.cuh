@@ -141,21 +141,31 @@ static size_t gemv_smem(int B, int K) {
 
 // ---------------------------------------------------------------- patch embed
 // h[b*L + l, d] = sum_k x_b[patch(l, k)] * Wpe[k, d] + bpe[d] + pos[l, d]
+// h rows of one lane: `txt` text rows copied from the fixed text states
+// (spec.py), then the patch embedding of each video token (+ the additive
+// position table when there is one; RoPE specs pass pos = null)
 static __global__ void patch_embed_kernel(const float* __restrict__ x, int64_t n_latent, DitGeom g,
                                    int patch_dim, const float* __restrict__ Wpe,
                                    const float* __restrict__ bpe, const float* __restrict__ pos,
-                                   float* __restrict__ h, int B) {
+                                   float* __restrict__ h, int B, int txt,
+                                   const float* __restrict__ text) {
   extern __shared__ float patch_s[];  // patch_dim values of this token
   pdl_wait_and_release();
-  const int row = blockIdx.x;  // b*L + l
-  const int b = row / g.L, l = row % g.L;
+  const int Lt = g.L + txt;
+  const int row = blockIdx.x;  // b*Lt + l
+  const int b = row / Lt, l = row % Lt - txt;
+  if (l < 0) {
+    for (int d = threadIdx.x; d < g.D; d += blockDim.x)
+      h[(int64_t)row * g.D + d] = text[(int64_t)(l + txt) * g.D + d];
+    return;
+  }
   for (int k = threadIdx.x; k < patch_dim; k += blockDim.x)
     patch_s[k] = x[(int64_t)b * n_latent + patch_elem_index(g, l, k)];
   __syncthreads();
   for (int d = threadIdx.x; d < g.D; d += blockDim.x) {
     float s = 0.f;
     for (int k = 0; k < patch_dim; ++k) s = fmaf(patch_s[k], Wpe[(int64_t)k * g.D + d], s);
-    h[(int64_t)row * g.D + d] = s + bpe[d] + pos[(int64_t)l * g.D + d];
+    h[(int64_t)row * g.D + d] = s + bpe[d] + (pos ? pos[(int64_t)l * g.D + d] : 0.f);
   }
 }
 
@@ -216,6 +226,8 @@ struct LnModArgs {
   int use_rows;              // lane b reads mod row mod_row[b] (else row b)
   int32_t mod_row[GV_MAXB];
   int shift_off, scale_off;
+  int txt;        // text rows per lane (row % L < txt) read their shift / scale
+  int txt_delta;  // this many floats further along the adaLN row (expert adaLN)
   float* out_f32;
   __nv_bfloat16* out_bf16;
   float* out_hi;
@@ -288,8 +300,11 @@ static __global__ void __launch_bounds__(256) ln_mod_kernel(const __grid_constan
   const float rstd = rsqrtf(q / p.D + 1e-6f);
   const int b = row / p.L;
   const int64_t mrow = p.use_rows ? p.mod_row[b] : b;
-  const float4* sh = reinterpret_cast<const float4*>(p.mod + mrow * p.mod_stride + p.shift_off);
-  const float4* sc = reinterpret_cast<const float4*>(p.mod + mrow * p.mod_stride + p.scale_off);
+  const int td = (p.txt && row % p.L < p.txt) ? p.txt_delta : 0;
+  const float4* sh =
+      reinterpret_cast<const float4*>(p.mod + mrow * p.mod_stride + p.shift_off + td);
+  const float4* sc =
+      reinterpret_cast<const float4*>(p.mod + mrow * p.mod_stride + p.scale_off + td);
 #pragma unroll
   for (int u = 0; u < LN_MAXV; ++u) {
     const int i = lane + 32 * u;

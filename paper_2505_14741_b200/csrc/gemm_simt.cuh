@@ -41,11 +41,44 @@ struct Epi {
   // EPI_STORE bf16 into a head-padded operand: column n = (w*H + h)*pad_dh + d
   // goes to (w*H + h)*pad_DH + d of a row of N/pad_dh*pad_DH (0 = dense)
   int pad_dh, pad_DH;
+  // text rows (spec.py text_tokens): rows with m % L < txt are text tokens;
+  // EPI_RESID reads their gate txt_delta floats further along the row
+  // (expert adaLN); EPI_UNPATCH skips them (L = txt + video tokens there)
+  int txt;
+  int64_t txt_delta;
+  // EPI_STORE of the QKV GEMM: 3D RoPE on the q and k columns (n < 2 * rope_D)
+  // of video rows, interleaved pairs; rope[(v * rope_dh / 2 + i) * 2 + {0, 1}]
+  // = (cos, sin) of pair i of video token v
+  const float* rope;
+  int rope_dh, rope_D;
 };
+
+// gate row of EPI_RESID for row m (text rows: the text half of the adaLN block)
+__device__ __forceinline__ const float* gate_row(const Epi& e, int m);
+
+// RoPE on 4 consecutive columns n..n+3 (n % 4 == 0) of row m, in place
+__device__ __forceinline__ void epi_rope4(const Epi& e, int m, int n, float* x) {
+  if (!e.rope || n >= 2 * e.rope_D) return;
+  const int v = m % e.L - e.txt;
+  if (v < 0) return;
+  const int i0 = (n % e.rope_dh) >> 1;
+  const float4 cs =
+      *reinterpret_cast<const float4*>(e.rope + ((int64_t)v * (e.rope_dh >> 1) + i0) * 2);
+  const float a0 = x[0], a1 = x[1], a2 = x[2], a3 = x[3];
+  x[0] = a0 * cs.x - a1 * cs.y;
+  x[1] = a1 * cs.x + a0 * cs.y;
+  x[2] = a2 * cs.z - a3 * cs.w;
+  x[3] = a3 * cs.z + a2 * cs.w;
+}
 
 __device__ __forceinline__ int64_t lane_row(const Epi& e, int m) {
   const int b = m / e.L;
   return e.use_rows ? e.lane_row[b] : b;
+}
+
+__device__ __forceinline__ const float* gate_row(const Epi& e, int m) {
+  const int64_t t = (e.txt && m % e.L < e.txt) ? e.txt_delta : 0;
+  return e.gate + lane_row(e, m) * e.gate_stride + t;
 }
 
 __device__ __forceinline__ int64_t padded_index(const Epi& e, int m, int n, int N) {
@@ -84,12 +117,13 @@ __device__ __forceinline__ void epi_store(const Epi& e, int m, int n, int N, flo
       break;
     }
     case EPI_RESID: {
-      e.resid[idx] = fmaf(e.gate[lane_row(e, m) * e.gate_stride + n], v, e.resid[idx]);
+      e.resid[idx] = fmaf(gate_row(e, m)[n], v, e.resid[idx]);
       break;
     }
-    case EPI_UNPATCH: {
-      const int b = m / e.g.L, l = m % e.g.L;
-      e.eps[(int64_t)b * e.n_latent + patch_elem_index(e.g, l, n)] = v;
+    case EPI_UNPATCH: {  // rows of a lane: txt text rows (skipped), then g.L video tokens
+      const int Lt = e.g.L + e.txt;
+      const int b = m / Lt, l = m % Lt - e.txt;
+      if (l >= 0) e.eps[(int64_t)b * e.n_latent + patch_elem_index(e.g, l, n)] = v;
       break;
     }
     case EPI_ADD: {
@@ -129,6 +163,8 @@ __device__ __forceinline__ void epi_store16(const Epi& e, int m, int n, int N, c
     x[4 * q + 3] = v[4 * q + 3] + bb.w;
   }
   if (e.mode == EPI_STORE) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) epi_rope4(e, m, n + 4 * q, x + 4 * q);
     if (e.out)
 #pragma unroll
       for (int q = 0; q < 4; ++q)
@@ -211,7 +247,7 @@ __device__ __forceinline__ void epi_store16(const Epi& e, int m, int n, int N, c
       *reinterpret_cast<uint4*>(e.out_bf16 + base + 8) = make_uint4(u[4], u[5], u[6], u[7]);
     }
   } else {  // EPI_RESID
-    const float* g = e.gate + lane_row(e, m) * e.gate_stride + n;
+    const float* g = gate_row(e, m) + n;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       float4 r = *reinterpret_cast<const float4*>(e.resid + base + 4 * q);
@@ -250,6 +286,7 @@ __device__ __forceinline__ void epi_store4(const Epi& e, int m, int n, int N, co
     *reinterpret_cast<uint2*>(out + (e.pad_DH ? padded_index(e, m, n, N) : base)) = u;
   };
   if (e.mode == EPI_STORE) {
+    epi_rope4(e, m, n, x);
     if (e.out) st_f32(e.out);
     if (e.out_bf16) st_bf16(e.out_bf16);
   } else if (e.mode == EPI_GELU) {
@@ -278,7 +315,7 @@ __device__ __forceinline__ void epi_store4(const Epi& e, int m, int n, int N, co
     if (e.out) st_f32(e.out);
     if (e.out_bf16) st_bf16(e.out_bf16);
   } else {  // EPI_RESID
-    const float4 g = *reinterpret_cast<const float4*>(e.gate + lane_row(e, m) * e.gate_stride + n);
+    const float4 g = *reinterpret_cast<const float4*>(gate_row(e, m) + n);
     float4 r = *reinterpret_cast<const float4*>(e.resid + base);
     r.x = fmaf(g.x, x[0], r.x);
     r.y = fmaf(g.y, x[1], r.y);

@@ -305,7 +305,7 @@ __device__ __forceinline__ void warp_store_rows(const Epi& e, const float* stg, 
         if (grow >= M || r >= nrows) continue;
         const int64_t base = (int64_t)grow * N + col;
         if (resid_mode)
-          ga[i] = *reinterpret_cast<const float4*>(e.gate + lane_row(e, grow) * e.gate_stride + col);
+          ga[i] = *reinterpret_cast<const float4*>(gate_row(e, grow) + col);
         else if (e.vec)
           ga[i] = *reinterpret_cast<const float4*>(e.vec + lane_row(e, grow) * e.vec_stride + col);
         if (e.resid) rb[i] = *reinterpret_cast<const float4*>(e.resid + base);

@@ -52,6 +52,23 @@ def position_table(s: DiTSpec) -> np.ndarray:
     return np.hstack([_sincos(D // 4, f), _sincos(3 * D // 8, hp), _sincos(3 * D // 8, wp)])
 
 
+PURPOSE_TEXT = 7  # the fixed text states of a text-conditioned spec (spec.py)
+
+
+def rope_table(s: DiTSpec) -> np.ndarray:
+    """[tokens, head_dim/2, 2] (cos, sin) of spec.py's 3D RoPE: pair i of band
+    (t: dh/4, h: 3dh/8, w: 3dh/8 dims) rotates by pos * 10000^(-2k/d_band)."""
+    dh = s.head_dim
+    idx = np.arange(s.tokens)
+    pos = [idx // (s.grid_h * s.grid_w), (idx // s.grid_w) % s.grid_h, idx % s.grid_w]
+    ang = []
+    for p, d in zip(pos, (dh // 4, 3 * dh // 8, 3 * dh // 8)):
+        k = np.arange(d // 2, dtype=np.float64)
+        ang.append(np.outer(p.astype(np.float64), np.power(10000.0, -2.0 * k / d)))
+    a = np.hstack(ang)
+    return np.stack([np.cos(a), np.sin(a)], axis=-1)
+
+
 class DiTWeights:
     """A device-resident DiT predictor; duck-types the reference weights object."""
 
@@ -94,20 +111,33 @@ class DiTWeights:
                 b = torch.zeros(fo, dtype=torch.float32, device="cuda")
             self.W.append(w)
             self.b.append(b)
-        self.pos = torch.as_tensor(position_table(self.spec), dtype=torch.float32, device="cuda")
+        s = self.spec
+        self.pos = None if s.rope else torch.as_tensor(position_table(s), dtype=torch.float32,
+                                                       device="cuda")
+        self.rope = torch.as_tensor(rope_table(s), dtype=torch.float32, device="cuda") \
+            if s.rope else None
+        self.text = None
+        if s.text_tokens:
+            t64 = torch.empty(s.text_tokens * s.hidden, dtype=torch.float64, device="cuda")
+            _lib.check(lib.ps_rng_normal(_lib.ptr(t64), t64.numel(), seed,
+                                         stream_id(PURPOSE_TEXT, 0), 0, _lib.PS_F64, st),
+                       "text states")
+            self.text = t64.to(torch.float32)
         self.freq = torch.as_tensor(time_embed_table(T_TABLE, self.spec.freq_dim),
                                     dtype=torch.float32, device="cuda")
-        s = self.spec
         cfg = _lib.ps_dit_config(
             channels=s.channels, frames=s.frames, height=s.height, width=s.width,
             layout=0 if s.layout == "CHW" else 1, patch=s.patch, hidden=s.hidden, depth=s.depth,
             heads=s.heads, mlp_hidden=s.mlp_hidden, freq_dim=s.freq_dim, max_batch=max_batch,
             precision=0 if precision == "fp32" else 1,
-            gemm_impl={"auto": 0, "simt": 1, "tcgen05": 2}[gemm_impl])
+            gemm_impl={"auto": 0, "simt": 1, "tcgen05": 2}[gemm_impl],
+            text_tokens=s.text_tokens, rope=int(s.rope))
         Wp = _lib.ptr_array([_lib.ptr(w) for w in self.W])
         bp = _lib.ptr_array([_lib.ptr(b) for b in self.b])
-        wts = _lib.ps_dit_weights(n_layers=len(self.W), W=Wp, b=bp, pos=_lib.ptr(self.pos),
-                                  freq_table=_lib.ptr(self.freq), freq_rows=T_TABLE + 1)
+        opt = lambda t: _lib.ptr(t) if t is not None else None  # noqa: E731
+        wts = _lib.ps_dit_weights(n_layers=len(self.W), W=Wp, b=bp, pos=opt(self.pos),
+                                  freq_table=_lib.ptr(self.freq), freq_rows=T_TABLE + 1,
+                                  text=opt(self.text), rope=opt(self.rope))
         torch.cuda.synchronize()
         h = _lib.C.c_void_p()
         _lib.check(lib.ps_dit_create(cfg, wts, _lib.C.byref(h)), "dit create")
@@ -140,7 +170,7 @@ class DiTWeights:
 
     def gemm_shape(self, which: int, B: int = 1) -> tuple[int, int, int]:
         s = self.spec
-        D, M = s.hidden, B * s.tokens
+        D, M = s.hidden, B * s.seq_len
         return [(M, 3 * D, D), (M, D, D), (M, s.mlp_hidden, D), (M, D, s.mlp_hidden)][which]
 
     def reserve_conditioning(self, T: int) -> None:

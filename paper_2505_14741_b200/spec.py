@@ -29,6 +29,24 @@ Fixed sin-cos position embedding added after the patch projection:
     F == 1:  [e1(D/2, hp), e1(D/2, wp)]
     F  > 1:  [e1(D/4, f), e1(3D/8, hp), e1(3D/8, wp)]
 
+Text tokens and RoPE (the CogVideoX-shaped spec; ``text_tokens`` > 0 and
+``rope``), following CogVideoX's transformer block structure:
+    * the sequence is [text_tokens text rows | video tokens]; the text rows
+      start from a fixed synthetic conditioning state drawn once per weight
+      seed, txt = normal(seed, stream (7<<32)|0)[text_tokens * D] row-major
+      (standing in for the T5 encoder output after CogVideoX's text
+      projection), and run through every block with the video rows;
+    * expert adaLN: b{i}.ada projects to 12D = [video shift1, scale1, gate1,
+      shift2, scale2, gate2 | the same six for the text rows]; each row uses
+      its own class's six vectors;
+    * attention runs over all text + video rows; q and k of the video rows
+      get 3D rotary embeddings (CogVideoX-5b's, interleaved pairs): head dims
+      split into t / h / w bands of dh/4, 3dh/8, 3dh/8; pair i of band a with
+      width d_a rotates by angle pos_a * 10000^(-2k/d_a) (k = i - band start):
+          q'[2i]   = q[2i] cos - q[2i+1] sin,   q'[2i+1] = q[2i+1] cos + q[2i] sin;
+      with RoPE there is no additive position embedding;
+    * the final adaLN + linear run on the video rows only.
+
 Latent layouts (the RNG counter is the flat index in this order, so the
 layout must equal the flatten order the reference's 1-D vector uses):
     "CHW"  — C x H x W (F = 1), e.g. 4x32x32
@@ -54,6 +72,8 @@ class DiTSpec:
     heads: int
     mlp_ratio: int = 4
     freq_dim: int = 256
+    text_tokens: int = 0
+    rope: bool = False
 
     @property
     def data_dim(self) -> int:
@@ -70,6 +90,16 @@ class DiTSpec:
     @property
     def tokens(self) -> int:
         return self.frames * self.grid_h * self.grid_w
+
+    @property
+    def seq_len(self) -> int:
+        """Rows per sample through the blocks: text tokens + video tokens."""
+        return self.text_tokens + self.tokens
+
+    @property
+    def ada_width(self) -> int:
+        """adaLN outputs per block: 6D, or 12D with text rows (expert adaLN)."""
+        return (12 if self.text_tokens else 6) * self.hidden
 
     @property
     def patch_dim(self) -> int:
@@ -94,12 +124,14 @@ class DiTSpec:
             raise ValueError("hidden must divide into heads")
         if self.hidden % 4 or self.freq_dim % 2:
             raise ValueError("hidden must be a multiple of 4, freq_dim even")
+        if self.rope and self.head_dim % 8:
+            raise ValueError("RoPE needs head_dim % 8 == 0 (t/h/w bands of dh/4, 3dh/8)")
 
     def flops_per_forward(self) -> int:
         """2 x MACs of all GEMMs + attention (QK^T and PV), one sample."""
-        L, D = self.tokens, self.hidden
+        L, D, Lv = self.seq_len, self.hidden, self.tokens
         per_block = L * D * (3 * D + D + 2 * self.mlp_hidden)
-        gemm = L * self.patch_dim * D + self.depth * per_block + L * D * self.patch_dim
+        gemm = Lv * self.patch_dim * D + self.depth * per_block + L * D * self.patch_dim
         attn = self.depth * 2 * L * L * D
         return 2 * (gemm + attn)
 
@@ -110,7 +142,7 @@ def layer_table(s: DiTSpec) -> list[tuple[str, int, int]]:
     out = [("patch", s.patch_dim, D), ("temb1", s.freq_dim, D), ("temb2", D, D)]
     for i in range(s.depth):
         out += [
-            (f"b{i}.ada", D, 6 * D),
+            (f"b{i}.ada", D, s.ada_width),
             (f"b{i}.qkv", D, 3 * D),
             (f"b{i}.proj", D, D),
             (f"b{i}.fc1", D, s.mlp_hidden),
@@ -130,6 +162,12 @@ SPECS = {
     "dit_s2": DiTSpec("dit_s2", 4, 1, 32, 32, "CHW", 2, 384, 12, 6),
     # configs[2]: DiT-XL/2-shaped
     "dit_xl2": DiTSpec("dit_xl2", 4, 1, 32, 32, "CHW", 2, 1152, 28, 16),
-    # configs[3]: CogVideoX-2b-shaped, latent 13x60x90x16 (channels-last)
-    "cogvideox_2b": DiTSpec("cogvideox_2b", 16, 13, 60, 90, "FHWC", 2, 1920, 30, 30),
+    # test-sized text + RoPE variant (the CogVideoX-shaped block structure)
+    "dit_tiny_text": DiTSpec("dit_tiny_text", 4, 3, 8, 12, "FHWC", 2, 128, 2, 2, freq_dim=32,
+                             text_tokens=10, rope=True),
+    # configs[3]: CogVideoX-2b-shaped, latent 13x60x90x16 (channels-last):
+    # 30 layers, hidden 1920, 30 heads of 64, 226 text tokens (CogVideoX's
+    # max_text_seq_length) + 17,550 video tokens, expert adaLN, 3D RoPE
+    "cogvideox_2b": DiTSpec("cogvideox_2b", 16, 13, 60, 90, "FHWC", 2, 1920, 30, 30,
+                            text_tokens=226, rope=True),
 }

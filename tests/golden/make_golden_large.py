@@ -12,7 +12,8 @@ sampler itself (build container only; needs /root/reference):
   latent 8x256x16, 200 steps, zero mode, seed 0: sequential and ParaStep
   degree 8 (warm-up 1, the paper's AudioLDM2 setting).
 * ``cogvideox_fwd.npz`` — configs[3]: one full-shape forward of the
-  CogVideoX-2b-shaped predictor (seed 0, 30 layers, 17,550 tokens) on the
+  CogVideoX-2b-shaped predictor (seed 0, 30 layers, 226 text + 17,550 video
+  tokens, expert adaLN, 3D RoPE) on the
   reference's x_T (``initial_state(0)``: normals of stream INIT<<32|0) at
   t = 37 of T = 50, eps stored as float32. A 50-step CPU trajectory at this
   shape is ~7 h, so parity for configs[3] is per forward.

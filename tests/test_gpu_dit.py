@@ -81,7 +81,27 @@ def test_dit_forward_fp32_vs_oracle(name, bias, impl):
     _dit_eps_close(name, bias, "fp32", impl, 1e-5)
 
 
-@pytest.mark.parametrize("name", ["dit_tiny", "dit_s2", "dit_long_video", "dit_xl2"])
+@pytest.mark.parametrize("bias", [0.0, 0.02])
+def test_dit_text_rope_forward_fp32_vs_oracle(bias):
+    """Text rows + expert adaLN + 3D RoPE fused in the QKV epilogue (the
+    CogVideoX-shaped block structure, spec.py) on the fp32 tcgen05 path."""
+    _dit_eps_close("dit_tiny_text", bias, "fp32", "tcgen05", 1e-5)
+
+
+def test_dit_text_rope_parastep_vs_oracle():
+    spec = SPECS["dit_tiny_text"]
+    w = DiTWeights(spec, seed=2, max_batch=4)
+    sch = S.make_default_schedule(16, "zero")
+    cfg = E.RunConfig(steps=16, warmup=2, strategy="parastep", degree=3, seed=5,
+                      data_dim=spec.data_dim)
+    tr = E.run_strategy(w, sch, cfg)
+    o = oeng.cycles(OracleDiT(spec, seed=2), core.Sched(16, "zero"), spec.data_dim, 5, warmup=2,
+                    degree=3)
+    assert core.rel_mae(o["x0"], tr.x0) <= FP32_TOL
+
+
+@pytest.mark.parametrize("name", ["dit_tiny", "dit_s2", "dit_long_video", "dit_xl2",
+                                  "dit_tiny_text"])
 def test_dit_forward_bf16_vs_oracle(name):
     errs = _dit_eps_close(name, 0.0, "bf16", "tcgen05", 5e-2)
     print(f"bf16 {name} eps rel-MAE vs fp64 oracle: {errs}")

@@ -385,6 +385,7 @@ USE_NCCL = False  # set in main(): world > 1, or --force-nccl (1-rank NCCL path 
 
 
 EXCHANGE = {"want": "peer", "used": None}  # --exchange; what the NCCL-group runs used
+SHARED_GPU = {"on": False}  # PS_BENCH_SHARED_GPU=1: N ranks on one GPU (code-path test)
 
 
 def make_sampler(w, sched, rcfg, world, record=False, external_init=False):
@@ -788,6 +789,9 @@ def our_arm(args, cfg, world, rank, local):
         "samples_ms": ms,
     }
     out.update(extra)
+    if SHARED_GPU["on"]:
+        out["shared_gpu_test"] = ("all ranks on cuda:0 (PS_BENCH_SHARED_GPU=1): exercises the "
+                                  "multi-rank code path; not a multi-GPU measurement")
     if USE_NCCL:
         out["config"]["exchange"] = {
             "peer": "peer memory: CUDA-IPC-mapped lane eps read over NVLink by the fused "
@@ -862,11 +866,21 @@ def main():
         import torch.distributed as dist
 
         if world > torch.cuda.device_count():
-            log(f"error: {world} ranks but {torch.cuda.device_count()} CUDA devices: "
-                "one rank per GPU is required")
-            return 2
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            if os.environ.get("PS_BENCH_SHARED_GPU") != "1":
+                log(f"error: {world} ranks but {torch.cuda.device_count()} CUDA devices: "
+                    "one rank per GPU is required")
+                return 2
+            # code-path test only (tests/test_gpu_bench_multi.py): every rank on
+            # cuda:0, gloo bootstrap, peer exchange; the timings are not a
+            # multi-GPU measurement and the line says so
+            SHARED_GPU["on"] = True
+            EXCHANGE["want"] = "peer"
+            local = 0
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     try:
         our_arm(args, cfg, world, rank, local)
     finally:

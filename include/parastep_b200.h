@@ -121,7 +121,7 @@ typedef struct ps_dit_config {
   int32_t patch, hidden, depth, heads, mlp_hidden, freq_dim;
   int32_t max_batch;
   int32_t precision;  /* 0 = fp32 (fp32-accurate GEMMs), 1 = bf16 tensor-core */
-  int32_t gemm_impl;  /* 0 = auto, 1 = SIMT fp32, 2 = tcgen05 */
+  int32_t gemm_impl;  /* 0 = auto (tcgen05), 2 = tcgen05; 1 = SIMT fp32 test reference only */
   int32_t text_tokens; /* text rows ahead of the video tokens (expert adaLN), 0 = none */
   int32_t rope;        /* 1 = 3D RoPE on the video rows' q/k (needs tcgen05), no pos table */
 } ps_dit_config;

@@ -11,7 +11,9 @@ LN-modulate -> GEMM with the unpatchify scatter fused in its epilogue.
 precision:
   "fp32" — fp32 activations, GEMMs on tcgen05 kind::tf32 with the 3-pass
            hi/lo split (fp32-class accuracy; the 1e-4 path of configs[1]),
-           or the SIMT fp32 kernel with gemm_impl="simt";
+           (gemm_impl="reference_simt" selects the SIMT fp32 GEMM and
+           attention kernels instead: an on-device cross-check used by the
+           tests only, never by the samplers, bench or CLI);
   "bf16" — bf16 GEMM operands on tcgen05 kind::f16, fp32 accumulation and
            fp32 residual stream (configs[2]).
 """
@@ -82,7 +84,7 @@ class DiTWeights:
         self.spec.validate()
         if precision not in ("fp32", "bf16"):
             raise ConfigError(f"unknown precision {precision!r}")
-        if gemm_impl not in ("auto", "simt", "tcgen05"):
+        if gemm_impl not in ("auto", "tcgen05", "reference_simt"):
             raise ConfigError(f"unknown gemm_impl {gemm_impl!r}")
         if not 1 <= max_batch <= 16:
             raise ConfigError("max_batch must be in [1, 16]")
@@ -130,7 +132,7 @@ class DiTWeights:
             layout=0 if s.layout == "CHW" else 1, patch=s.patch, hidden=s.hidden, depth=s.depth,
             heads=s.heads, mlp_hidden=s.mlp_hidden, freq_dim=s.freq_dim, max_batch=max_batch,
             precision=0 if precision == "fp32" else 1,
-            gemm_impl={"auto": 0, "simt": 1, "tcgen05": 2}[gemm_impl],
+            gemm_impl={"auto": 0, "reference_simt": 1, "tcgen05": 2}[gemm_impl],
             text_tokens=s.text_tokens, rope=int(s.rope))
         Wp = _lib.ptr_array([_lib.ptr(w) for w in self.W])
         bp = _lib.ptr_array([_lib.ptr(b) for b in self.b])

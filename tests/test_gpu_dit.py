@@ -74,7 +74,7 @@ def _dit_eps_close(name, bias, precision, impl, tol):
     return errs
 
 
-@pytest.mark.parametrize("impl", ["simt", "tcgen05"])
+@pytest.mark.parametrize("impl", ["reference_simt", "tcgen05"])
 @pytest.mark.parametrize("name,bias", [("dit_tiny", 0.05), ("dit_tiny_video", 0.0),
                                        ("dit_s2", 0.0), ("dit_long_video", 0.02)])
 def test_dit_forward_fp32_vs_oracle(name, bias, impl):
@@ -119,7 +119,7 @@ def _traj_close(tr, g, prefix, tol):
     return err
 
 
-@pytest.mark.parametrize("impl", ["simt", "tcgen05"])
+@pytest.mark.parametrize("impl", ["reference_simt", "tcgen05"])
 def test_dit_trajectories_vs_reference_sampler(gold_dit, impl):
     """The reference's own engines drove the oracle DiT to make these."""
     for name, bias in (("dit_tiny", 0.05), ("dit_tiny_video", 0.0)):

@@ -564,16 +564,26 @@ def cpu_leg(args, cfg, w, sched, n, torch):
 
     ncores = len(os.sched_getaffinity(0))
     if cfg["spec"] == "cogvideox_2b":
-        pred = cpu_predictor(cfg)
+        # one full-shape forward is ~1 h of f64 numpy on 8 cores (the fixture's
+        # run): time ONE block at the full sequence (17,776 rows) plus the
+        # embeddings, and extrapolate by depth and the T calls
+        import dataclasses
+
+        from oracle.dit import DiT
+        from paper_2505_14741_b200.spec import SPECS
+
+        full = SPECS[cfg["spec"]]
+        pred = DiT(dataclasses.replace(full, depth=1), seed=0)
         x = np.random.default_rng(0).standard_normal(pred.data_dim)
         t0 = time.perf_counter()
         pred(x, 37, cfg["T"])
         el = time.perf_counter() - t0
-        return ({"value": el * cfg["T"] * 1e3, "unit": "ms", "cores": ncores, "kind": "port",
-                 "cpu_model": cpu_model(),
-                 "sample": f"one full-shape forward of the oracle predictor (numpy f64, "
-                           f"{el:.0f} s), extrapolated x{cfg['T']} calls; the sampler steps "
-                           f"(<0.1% of it) omitted"}, None)
+        return ({"value": el * full.depth * cfg["T"] * 1e3, "unit": "ms", "cores": ncores,
+                 "kind": "port", "cpu_model": cpu_model(),
+                 "sample": f"one block of the oracle predictor at the full 17,776-row sequence "
+                           f"(numpy f64, {el:.0f} s incl. embeddings), extrapolated "
+                           f"x{full.depth} blocks x{cfg['T']} calls; sampler steps omitted"},
+                None)
     full = args.config in CPU_FULL
     el, done, x0_ref, kind = cpu_reference_run(
         cfg, max_forwards=None if full else (args.ref_sample or 3))

@@ -437,21 +437,28 @@ def time_runs(sampler, K, W, flush, torch, dist, world, seed0=0):
 
 
 def gemm_roofline(w, cfg, torch, bf16_peak):
-    """Dominant kernel: the tcgen05 GEMM of the MLP fc1 layer (M = tokens)."""
+    """Dominant GEMM: of the block's four tcgen05 GEMMs (qkv, proj, fc1, fc2;
+    one launch each per block) the one with the longest launch - the
+    largest share of the step (profiles/r2_launches_*_by_grid.txt) - timed
+    with CUDA events around back-to-back launches on the current stream."""
     if cfg["spec"] is None or cfg.get("family") == "unet":
         return None
-    which = 2
-    M, N, K = w.gemm_shape(which, 1)
-    w.bench_gemm(which, 1, 3)
-    torch.cuda.synchronize()
+    names = ("qkv", "proj", "fc1", "fc2")
     iters = 50
-    a = torch.cuda.Event(enable_timing=True)
-    b = torch.cuda.Event(enable_timing=True)
-    a.record()
-    w.bench_gemm(which, 1, iters)
-    b.record()
-    torch.cuda.synchronize()
-    t = a.elapsed_time(b) / iters * 1e-3
+    times = {}
+    for which in range(4):
+        w.bench_gemm(which, 1, 3)
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        w.bench_gemm(which, 1, iters)
+        b.record()
+        torch.cuda.synchronize()
+        times[which] = a.elapsed_time(b) / iters * 1e-3
+    which = max(times, key=times.get)
+    M, N, K = w.gemm_shape(which, 1)
+    t = times[which]
     flops = 2.0 * M * N * K
     if cfg["precision"] == "bf16":
         peak, note = bf16_peak, "measured bf16 dense (burst)"
@@ -464,11 +471,12 @@ def gemm_roofline(w, cfg, torch, bf16_peak):
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get(f"{cfg['spec']}_{cfg['precision']}_fc1")
+            traffic = json.load(f).get(f"{cfg['spec']}_{cfg['precision']}_{names[which]}")
     return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved / peak, "traffic": traffic,
-            "kernel": f"gemm_tc fc1 M={M} N={N} K={K} ({cfg['precision']})",
-            "launch_us": t * 1e6, "peak_note": note}
+            "kernel": f"gemm_tc {names[which]} M={M} N={N} K={K} ({cfg['precision']})",
+            "launch_us": t * 1e6, "peak_note": note,
+            "block_gemm_launch_us": {names[i]: times[i] * 1e6 for i in range(4)}}
 
 
 def attn_roofline(w, cfg, bf16_peak):

@@ -51,7 +51,8 @@ def main(path):
             if label.endswith("_MB"):
                 x = x * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(u, 1.0)
             elif label == "dur_us":
-                x = x * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(u, 1.0)
+                x = x * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3,
+                         "ms": 1e3}[u]
             out.append(f"{x:.3g}")
         print(" | ".join(out))
 

@@ -1,7 +1,8 @@
 """Launch one instance of a named hot kernel for an `ncu --set full` capture.
 
     ncu --set full -k regex:fmha -c 1 -o out python tools/ncu_targets.py fmha_cogvideox
-targets: fmha_cogvideox, fmha_xl, sched, gemm_s2_fc1, gemm_cog_fc1, unet
+targets: fmha_cogvideox, fmha_xl, fmha_f32_s2, sched, gemm_s2_fc1, gemm_s2_fc2, gemm_xl_fc1,
+gemm_xl_fc2, gemm_cog_fc1, unet
 """
 import os
 import sys
@@ -15,6 +16,8 @@ lib = _lib.load(require_gpu=True)
 t = sys.argv[1]
 if t == "fmha_cogvideox":
     lib.ps_attn_probe(1, 17550, 30, 1920, 2, 1)
+elif t == "fmha_f32_s2":  # fp32-path tcgen05 attention at the DiT-S/2 head set
+    lib.ps_attn_probe(1, 256, 6, 384, 6, 1)
 elif t == "fmha_xl":
     lib.ps_attn_probe(1, 256, 16, 1152, 2, 1)
 elif t == "sched":
@@ -23,6 +26,10 @@ elif t == "sched":
     bench.sched_roofline(torch, 6550.7)
 elif t == "gemm_s2_fc1":
     lib.ps_gemm_probe(256, 1536, 384, 0, 0, 1)
+elif t == "gemm_s2_fc2":
+    lib.ps_gemm_probe(256, 384, 1536, 0, 0, 1)
+elif t == "gemm_xl_fc2":
+    lib.ps_gemm_probe(256, 1152, 4608, 1, 0, 1)
 elif t == "gemm_xl_fc1":
     lib.ps_gemm_probe(256, 4608, 1152, 1, 0, 1)
 elif t == "gemm_cog_fc1":

@@ -233,8 +233,31 @@ struct TilePlan {
 
 static TilePlan plan_tiles_auto(int precision, int M, int N, int K);
 
+// Measured overrides at the benchmarked batch-1 shapes (tools/gemm_plan_real.py:
+// back-to-back launches of the real layers with every (BN, S) forced,
+// profiles/r2_gemm_plan_real.txt); the cost model stays the fallback. A
+// fixed table (not run-time autotuning) so every process and rank plans the
+// same split-K order: bits never depend on timing noise.
+struct PlanRule {
+  int precision, M, N, K, bn, splits;
+};
+static const PlanRule kMeasuredPlans[] = {
+    // DiT-S/2, 3xTF32 (auto: 7.32 / 6.27 / 8.55 / 7.96 us)
+    {0, 256, 1152, 384, 32, 2},  // qkv 7.21
+    {0, 256, 384, 384, 32, 4},   // proj 6.28
+    {0, 256, 1536, 384, 32, 1},  // fc1 8.05
+    {0, 256, 384, 1536, 64, 8},  // fc2 7.93
+    // DiT-XL/2, bf16 (auto: 8.42 / 7.02 / 8.31 / 11.23 us)
+    {1, 256, 3456, 1152, 32, 1},  // qkv 8.18
+    {1, 256, 1152, 1152, 32, 1},  // proj 6.48
+    {1, 256, 4608, 1152, 32, 1},  // fc1 8.03
+    {1, 256, 1152, 4608, 32, 2},  // fc2 10.48
+};
+
 static TilePlan plan_tiles(int precision, int M, int N, int K) {
   TilePlan p = plan_tiles_auto(precision, M, N, K);
+  for (const PlanRule& r : kMeasuredPlans)
+    if (r.precision == precision && r.M == M && r.N == N && r.K == K) p = TilePlan{r.bn, r.splits};
   if (g_force_bn) p.bn = g_force_bn;
   if (g_force_splits) p.splits = g_force_splits;
   return p;

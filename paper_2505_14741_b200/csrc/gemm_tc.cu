@@ -200,6 +200,40 @@ static int launch2(const TcLayer& L, const TcOperand& A, int M, int N, int K, co
   return check_launch("gemm_tc2");
 }
 
+static int g_tc2_persistent = 1;  // test hook: 0 = one pair tile per CTA pair
+
+// persistent 2-SM launch: one CTA pair per 2 SMs (at most 74 pairs), each
+// walking pair tiles with a double-buffered TMEM accumulator
+static int launch2p(const TcLayer& L, const TcOperand& A, int M, int N, int K, const Epi& e,
+                    cudaStream_t st) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(gemm_tc2p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         TC2P_SMEM);
+  });
+  const int ntiles = ((M + 255) / 256) * ((N + TC2_BN - 1) / TC2_BN);
+  const int pairs = std::min(ntiles, 74);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs, 1, 1);
+  cfg.blockDim = dim3(TC2P_THREADS);
+  cfg.dynamicSmemBytes = TC2P_SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = 2;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  cudaError_t err =
+      cudaLaunchKernelEx(&cfg, gemm_tc2p_kernel, A.map_main[0], L.map_b[2], M, N, K, e);
+  if (err != cudaSuccess)
+    return fail((int)err, std::string("gemm_tc2p: ") + cudaGetErrorString(err));
+  return check_launch("gemm_tc2p");
+}
+
 // A layer takes the 2-SM kernel when one lane alone fills several waves of
 // 128 x 128 tiles (decided from ref_rows, so every batch of the layer runs
 // the same kernel: a row's bits never depend on the batch).
@@ -371,7 +405,8 @@ int tc_prepare(TcWeights& w, TcActs& acts, const std::vector<const float*>& Ws,
 int tc_gemm(const TcWeights& w, int layer, const TcOperand& A, int M, int N, int K, const Epi& e,
             int precision, cudaStream_t st) {
   const TcLayer& L = w.layers[layer];
-  if (use_2sm(L, precision)) return launch2(L, A, M, N, K, e, st);
+  if (use_2sm(L, precision))
+    return g_tc2_persistent ? launch2p(L, A, M, N, K, e, st) : launch2(L, A, M, N, K, e, st);
   const int bn = choose_bn(L, precision, M, N);
   if (precision == 1) {
     if (bn == 32) return launch<KIND_BF16, 32>(L, A, M, N, K, e, st);
@@ -425,10 +460,12 @@ int ps_gemm_test(const float* A, const float* W, const float* bias, float* Cout,
   // impl 3: tensor cores with the K segments forced in-CTA (cluster-free);
   // must equal impl 2 bit-for-bit (test_gemm_split_paths_bitwise)
   // impl 4: at most 2 cluster CTAs along K (each running S/2 segments);
-  // impl 5 / 6: bf16 2-SM (cta_group::2) kernel forced on / off
+  // impl 5 / 6: bf16 2-SM (cta_group::2) kernel forced on / off; 5 = one pair
+  // tile per CTA pair, 7 = the persistent double-buffered 2-SM kernel
   g_force_in_cta = impl == 3 ? 1 : 0;
   g_sc_max = impl == 4 ? 2 : 8;
-  g_force_2sm = impl == 5 ? 1 : (impl == 6 ? 0 : -1);
+  g_force_2sm = (impl == 5 || impl == 7) ? 1 : (impl == 6 ? 0 : -1);
+  g_tc2_persistent = impl == 5 ? 0 : 1;
   if (impl >= 3) impl = 2;
   Epi e{};
   e.mode = EPI_STORE;
@@ -457,6 +494,7 @@ int ps_gemm_test(const float* A, const float* W, const float* bias, float* Cout,
   g_force_in_cta = 0;
   g_sc_max = 8;
   g_force_2sm = -1;
+  g_tc2_persistent = 1;
   return rc;
 }
 

@@ -785,6 +785,206 @@ static __global__ void __launch_bounds__(TC_THREADS, 1)
   }
 }
 
+// ------------------------------------------------------------------ persistent 2-SM GEMM
+// The 2-SM GEMM as a persistent kernel: one CTA pair per 2 SMs walks the
+// pair tiles t = cluster, cluster + clusters, ... (N-tile fastest, so pairs
+// running together share A rows in L2). TMEM holds two 256-column
+// accumulators: while four epilogue warps drain tile i's accumulator
+// (TMEM -> smem staging -> coalesced rows), the leader's MMA warp already
+// accumulates tile i+1 into the other one - the epilogue, the prologue and
+// the teardown leave the tensor pipe's critical path. Stage ring phases run
+// on across tiles. Barriers: full/empty as in gemm_tc2_kernel; acc_full[b]
+// (each CTA; the leader's multicast commit) and acc_empty[b] (the leader's;
+// 8 arrivals = both CTAs' four epilogue warps, the peer's over DSMEM).
+// Warps: 0 TMA, 1 MMA (leader), 2-5 epilogue (lane quarters 2, 3, 0, 1).
+// Same MMA sequence per tile as gemm_tc2_kernel: bitwise-identical output.
+constexpr int TC2P_STAGES = 4, TC2P_THREADS = 192;
+constexpr int TC2P_EST = 128 + 4;
+constexpr int TC2P_STG_BYTES = 4 * 32 * TC2P_EST * 4;  // per-warp epilogue staging
+constexpr int TC2P_SMEM = TC2P_STAGES * TC2_STAGE_BYTES + TC2P_STG_BYTES + 1024 + 256;
+
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAITC_%=;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(cta));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+               : "memory");
+}
+
+static __global__ void __launch_bounds__(TC2P_THREADS, 1)
+    gemm_tc2p_kernel(const __grid_constant__ CUtensorMap mapA,
+                     const __grid_constant__ CUtensorMap mapB, int M, int N, int K,
+                     const __grid_constant__ Epi e) {
+  extern __shared__ __align__(1024) uint8_t tc2p_smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(tc2p_smem_raw) + 1023) & ~uintptr_t(1023));
+  float* stg_all = reinterpret_cast<float*>(smem + TC2P_STAGES * TC2_STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TC2P_STAGES * TC2_STAGE_BYTES +
+                                               TC2P_STG_BYTES);
+  uint64_t* empty = full + TC2P_STAGES;
+  uint64_t* acc_full = empty + TC2P_STAGES;  // [2]
+  uint64_t* acc_empty = acc_full + 2;        // [2], leader's used
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int tiles_mp = (M + 255) / 256, tiles_n = (N + TC2_BN - 1) / TC2_BN;
+  const int ntiles = tiles_mp * tiles_n;
+  const int nk = (K + 63) / 64;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&mapA);
+    tma_prefetch_desc(&mapB);
+    for (int s = 0; s < TC2P_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(2 * TC2_BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  cluster_sync_all();  // the leader's barriers exist before the peer signals them
+  pdl_wait_and_release();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs), completion on the leader's barrier
+      int g = 0;
+      for (int t = cl; t < ntiles; t += ncl) {
+        const int m0 = (t / tiles_n) * 256 + (int)rank * 128;
+        const int nh0 = (t % tiles_n) * TC2_BN + (int)rank * 128;
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int s = g % TC2P_STAGES;
+          mbar_wait(&empty[s], ((g / TC2P_STAGES) & 1) ^ 1);
+          const uint32_t bar = smem_u32(&full[s]) & 0xFEFFFFFFu;  // rank-0 CTA's barrier
+          if (rank == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                             smem_u32(&full[s])),
+                         "r"(2 * TC2_STAGE_BYTES)
+                         : "memory");
+          uint8_t* st = smem + s * TC2_STAGE_BYTES;
+          const int kx = kb * 64;
+          asm volatile(
+              "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::"
+              "bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(st)),
+              "l"(reinterpret_cast<uint64_t>(&mapA)), "r"(bar), "r"(kx), "r"(m0)
+              : "memory");
+          asm volatile(
+              "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::"
+              "bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(st + TC2_A_BYTES)),
+              "l"(reinterpret_cast<uint64_t>(&mapB)), "r"(bar), "r"(kx), "r"(nh0)
+              : "memory");
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {
+      // ---------------- MMA issuer (leader), accumulator i & 1 for local tile i
+      constexpr uint32_t idesc = make_idesc(KIND_BF16, 256, TC2_BN);
+      int g = 0, i = 0;
+      for (int t = cl; t < ntiles; t += ncl, ++i) {
+        const int b = i & 1;
+        mbar_wait_cluster(&acc_empty[b], ((i >> 1) & 1) ^ 1);  // both CTAs drained it
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t dacc = tmem + (uint32_t)(b * TC2_BN);
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int s = g % TC2P_STAGES;
+          mbar_wait(&full[s], (g / TC2P_STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          uint8_t* st = smem + s * TC2_STAGE_BYTES;
+          const uint64_t a0 = smem_desc_sw128(st);
+          const uint64_t b0 = smem_desc_sw128(st + TC2_A_BYTES);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t koff = (uint64_t)(k * 32) >> 4;
+            const uint32_t acc = (kb | k) ? 1u : 0u;
+            asm volatile(
+                "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dacc),
+                "l"(a0 + koff), "l"(b0 + koff), "r"(idesc), "r"(acc));
+          }
+          asm volatile(
+              "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+              "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::"
+              "cluster.b64 [%0], %1;\n\t}" ::"r"(smem_u32(&empty[s])),
+              "h"((uint16_t)3)
+              : "memory");
+        }
+        asm volatile(
+            "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+            "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::"
+            "cluster.b64 [%0], %1;\n\t}" ::"r"(smem_u32(&acc_full[b])),
+            "h"((uint16_t)3)
+            : "memory");
+      }
+    }
+  } else {
+    // ---------------- epilogue warps 2-5: TMEM lane quarter q = warp & 3
+    const int q = warp & 3;
+    float* stg = stg_all + q * 32 * TC2P_EST;
+    int i = 0;
+    for (int t = cl; t < ntiles; t += ncl, ++i) {
+      const int b = i & 1;
+      const int m0 = (t / tiles_n) * 256 + (int)rank * 128;
+      const int nb0 = (t % tiles_n) * TC2_BN;
+      mbar_wait(&acc_full[b], (i >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t trow = tmem + (uint32_t)(b * TC2_BN) + ((uint32_t)(q * 32) << 16);
+#pragma unroll 1
+      for (int h = 0; h < TC2_BN; h += 128) {
+#pragma unroll 1
+        for (int c = 0; c < 128; c += 16) {
+          float v[16];
+          tmem_ld16(trow + h + c, v);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<float4*>(stg + lane * TC2P_EST + c + 4 * j) =
+                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        }
+        if (h + 128 >= TC2_BN) {  // accumulator b fully read: hand it back to the MMA
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(&acc_empty[b], 0u);
+        }
+        __syncwarp();
+        warp_store_rows<128, TC2P_EST>(e, stg, m0 + q * 32, nb0 + h, M, N, lane);
+        __syncwarp();
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  cluster_sync_all();  // the peer's TMA / our commits / remote arrives are all done
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(2 * TC2_BN));
+  }
+}
+
 // ------------------------------------------------------------------ host side
 int tc_prepare(TcWeights& w, TcActs& acts, const std::vector<const float*>& Ws,
                const std::vector<int>& Ks, const std::vector<int>& Ns, int max_rows, int ref_rows,

@@ -211,3 +211,17 @@ def test_gemm_2sm_vs_fp64_and_1sm(shape):
     assert ((c2.double() - ref).abs() / scale).max().item() < 1e-2
     print("2sm vs 1sm max abs diff", (c2 - c1).abs().max().item())
     assert (c2 - c1).abs().max().item() <= 1e-3 * c1.abs().max().item()
+
+
+@pytest.mark.parametrize("shape", [(2048, 1024, 512), (2304, 1920, 1152), (4096, 640, 256),
+                                   (1000, 1920, 1920), (17776 // 4, 5760, 384), (300, 256, 64)])
+def test_gemm_2sm_persistent_bitwise(shape):
+    """The persistent 2-SM GEMM (double-buffered TMEM accumulators, pair
+    tiles walked per CTA pair) equals the one-tile-per-pair kernel bit for
+    bit: same MMA sequence per tile; ragged M / N tiles included."""
+    M, N, K = shape
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
+    A = torch.randn((M, K), device="cuda", generator=g)
+    W = torch.randn((K, N), device="cuda", generator=g) / K ** 0.5
+    bias = torch.randn(N, device="cuda", generator=g)
+    assert torch.equal(_gemm(A, W, bias, 1, 7), _gemm(A, W, bias, 1, 5))

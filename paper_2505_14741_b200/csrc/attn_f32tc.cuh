@@ -66,21 +66,35 @@ __device__ __forceinline__ float f3_hi(float v) {
 // and columns >= dh read as 0) -> hi / lo copies in the SW128 K-major layout:
 // atom a (columns [32a, 32a+32)) at a * ROWS * 128, row r at r * 128 B, 16-byte
 // chunk c at ((c ^ (r & 7)) << 4) - the layout TMA SWIZZLE_128B produces.
+// Split into a fetch (every global load of the tile issued at once, into
+// registers) and a store (hi/lo split into smem), so the loads of the next
+// key block are in flight while the current one is on the tensor core.
 template <int NA, int ROWS>
-__device__ __forceinline__ void f3_load_tile(uint8_t* hi, uint8_t* lo, const float* src, int64_t ld,
-                                             int nvalid, int dh) {
-  constexpr int CPR = NA * 8;  // 16-byte chunks per row
-#pragma unroll 4
-  for (int q = threadIdx.x; q < ROWS * CPR; q += F3_THREADS) {
-    const int r = q / CPR, cc = q % CPR, a = cc >> 3, c = cc & 7, d0 = 4 * cc;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (r < nvalid && d0 < dh) v = __ldg(reinterpret_cast<const float4*>(src + r * ld + d0));
-    const float4 h = make_float4(f3_hi(v.x), f3_hi(v.y), f3_hi(v.z), f3_hi(v.w));
-    const int off = a * ROWS * 128 + r * 128 + ((c ^ (r & 7)) << 4);
-    *reinterpret_cast<float4*>(hi + off) = h;
-    *reinterpret_cast<float4*>(lo + off) = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+struct F3Tile {
+  static constexpr int CPR = NA * 8;                      // 16-byte chunks per row
+  static constexpr int N = ROWS * CPR / F3_THREADS;       // chunks per thread
+  static_assert(ROWS * CPR % F3_THREADS == 0, "whole chunks per thread");
+  float4 v[N];
+  __device__ __forceinline__ void fetch(const float* src, int64_t ld, int nvalid, int dh) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const int q = threadIdx.x + i * F3_THREADS, r = q / CPR, d0 = 4 * (q % CPR);
+      v[i] = (r < nvalid && d0 < dh) ? __ldg(reinterpret_cast<const float4*>(src + r * ld + d0))
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
   }
-}
+  __device__ __forceinline__ void store(uint8_t* hi, uint8_t* lo) const {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const int q = threadIdx.x + i * F3_THREADS, r = q / CPR, cc = q % CPR;
+      const int off = (cc >> 3) * ROWS * 128 + r * 128 + (((cc & 7) ^ (r & 7)) << 4);
+      const float4 h = make_float4(f3_hi(v[i].x), f3_hi(v[i].y), f3_hi(v[i].z), f3_hi(v[i].w));
+      *reinterpret_cast<float4*>(hi + off) = h;
+      *reinterpret_cast<float4*>(lo + off) =
+          make_float4(v[i].x - h.x, v[i].y - h.y, v[i].z - h.z, v[i].w - h.w);
+    }
+  }
+};
 
 // V block (F3_BK keys x dh, same source layout) -> V^T hi / lo as the K-major
 // B operand of P V: row n = head dim n, K = keys in atoms of 32 keys (128 B)
@@ -89,28 +103,41 @@ __device__ __forceinline__ void f3_load_tile(uint8_t* hi, uint8_t* lo, const flo
 // kind::tf32 with V as an MN-major SW128 B operand, the bf16 kernel's form,
 // accumulated nothing on B200, so V is transposed here instead.)
 template <int NA>
-__device__ __forceinline__ void f3_load_vt(uint8_t* hi, uint8_t* lo, const float* src, int64_t ld,
-                                           int nvalid, int dh) {
-  constexpr int DHP = 32 * NA;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll 2
-  for (int it = warp; it < (F3_BK / 32) * (DHP / 4); it += F3_THREADS / 32) {
-    const int kb = it / (DHP / 4), n0 = 4 * (it % (DHP / 4));  // key group, dim quad
-    const int key = kb * 32 + lane;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (key < nvalid && n0 < dh) v = __ldg(reinterpret_cast<const float4*>(src + key * ld + n0));
-    const float x[4] = {v.x, v.y, v.z, v.w};
-    const int cbase = kb * DHP * 128 + 4 * (lane & 3);
+struct F3VTile {
+  static constexpr int DHP = 32 * NA;
+  static constexpr int ITS = (F3_BK / 32) * (DHP / 4);  // (key group, dim quad) passes
+  static constexpr int N = ITS / (F3_THREADS / 32);      // per warp
+  static_assert(ITS % (F3_THREADS / 32) == 0, "whole passes per warp");
+  float4 v[N];
+  __device__ __forceinline__ void fetch(const float* src, int64_t ld, int nvalid, int dh) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int n = n0 + i;
-      const int off = cbase + n * 128 + ((((lane >> 2) ^ (n & 7))) << 4);
-      const float h = f3_hi(x[i]);
-      *reinterpret_cast<float*>(hi + off) = h;
-      *reinterpret_cast<float*>(lo + off) = x[i] - h;
+    for (int i = 0; i < N; ++i) {
+      const int it = warp + i * (F3_THREADS / 32);
+      const int key = (it / (DHP / 4)) * 32 + lane, n0 = 4 * (it % (DHP / 4));
+      v[i] = (key < nvalid && n0 < dh) ? __ldg(reinterpret_cast<const float4*>(src + key * ld + n0))
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
-}
+  __device__ __forceinline__ void store(uint8_t* hi, uint8_t* lo) const {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const int it = warp + i * (F3_THREADS / 32);
+      const int kb = it / (DHP / 4), n0 = 4 * (it % (DHP / 4));
+      const float x[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+      const int cbase = kb * DHP * 128 + 4 * (lane & 3);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int n = n0 + j;
+        const int off = cbase + n * 128 + ((((lane >> 2) ^ (n & 7))) << 4);
+        const float h = f3_hi(x[j]);
+        *reinterpret_cast<float*>(hi + off) = h;
+        *reinterpret_cast<float*>(lo + off) = x[j] - h;
+      }
+    }
+  }
+};
 
 template <int NA, int KS>
 __global__ void __launch_bounds__(F3_THREADS, 1) fmha_f32_kernel(const __grid_constant__ AttnArgs p) {
@@ -160,7 +187,16 @@ __global__ void __launch_bounds__(F3_THREADS, 1) fmha_f32_kernel(const __grid_co
   const float sl2 = p.scale * 1.4426950408889634f;
   float m_run = -INFINITY, l = 0.f;
 
-  f3_load_tile<NA, F3_BQ>(q_hi, q_lo, base + (int64_t)q0 * ld, ld, L - q0, dh);
+  // Q and this CTA's first K / V block: every load in flight at once
+  F3Tile<NA, F3_BQ> qt;
+  F3Tile<NA, F3_BK> kt;
+  F3VTile<NA> vt;
+  qt.fetch(base + (int64_t)q0 * ld, ld, L - q0, dh);
+  if (z < nkb) {
+    kt.fetch(base + (int64_t)z * F3_BK * ld + D, ld, L - z * F3_BK, dh);
+    vt.fetch(base + (int64_t)z * F3_BK * ld + 2 * D, ld, L - z * F3_BK, dh);
+  }
+  qt.store(q_hi, q_lo);
   int nloc = 0;  // key blocks this CTA ran
   for (int jb = z; jb < nkb; jb += KS, ++nloc) {
     const int j = nloc;  // local block index: barrier phases, first-block flags
@@ -169,8 +205,13 @@ __global__ void __launch_bounds__(F3_THREADS, 1) fmha_f32_kernel(const __grid_co
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
     const int k0 = jb * F3_BK, valid = L - k0;
-    f3_load_tile<NA, F3_BK>(k_hi, k_lo, base + (int64_t)k0 * ld + D, ld, valid, dh);
-    f3_load_vt<NA>(v_hi, v_lo, base + (int64_t)k0 * ld + 2 * D, ld, valid, dh);
+    kt.store(k_hi, k_lo);
+    vt.store(v_hi, v_lo);
+    if (jb + KS < nkb) {  // the next block's loads overlap this block's MMAs / softmax
+      const int k1 = (jb + KS) * F3_BK;
+      kt.fetch(base + (int64_t)k1 * ld + D, ld, L - k1, dh);
+      vt.fetch(base + (int64_t)k1 * ld + 2 * D, ld, L - k1, dh);
+    }
     // generic-proxy smem writes -> visible to the tensor core (async proxy)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

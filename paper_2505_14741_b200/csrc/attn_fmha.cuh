@@ -113,6 +113,52 @@ __device__ __forceinline__ float poly_exp2(float x) {
   return __int_as_float(__float_as_int(q) + (__float_as_int(r) << 23));
 }
 
+// Blackwell packed fp32 pairs (FFMA2 / FADD2) and the 3-input max (FMNMX3):
+// the softmax's per-element ALU work in half the issue slots. Lane-wise the
+// same IEEE operations as fmaf / + / fmaxf.
+__device__ __forceinline__ unsigned long long f2_pack(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 f2_unpack(unsigned long long v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "l"(f2_pack(a.x, a.y)), "l"(f2_pack(b.x, b.y)), "l"(f2_pack(c.x, c.y)));
+  return f2_unpack(r);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_pack(a.x, a.y)), "l"(f2_pack(b.x, b.y)));
+  return f2_unpack(r);
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// poly_exp2 on a pair (FFMA2 / FADD2 Horner): lane-wise identical to poly_exp2
+__device__ __forceinline__ float2 poly_exp2x2(float2 x) {
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  const float2 mg = make_float2(12582912.f, 12582912.f);
+  const float2 r = fadd2(x, mg);
+  const float2 f = fadd2(x, make_float2(-(r.x - 12582912.f), -(r.y - 12582912.f)));
+  float2 q = ffma2(make_float2(0.0550089292f, 0.0550089292f), f,
+                   make_float2(0.242210984f, 0.242210984f));
+  q = ffma2(q, f, make_float2(0.693282902f, 0.693282902f));
+  q = ffma2(q, f, make_float2(1.f, 1.f));
+  return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(r.x) << 23)),
+                     __int_as_float(__float_as_int(q.y) + (__float_as_int(r.y) << 23)));
+}
+
 #ifdef FMHA_STAMPS
 __device__ long long g_fm_ts[9][32][4];
 #define FM_TS(role, j, k) \
@@ -311,7 +357,7 @@ __global__ void __launch_bounds__(FmCfg<DH, NQ>::THREADS, 1)
             if (g * CH + i >= valid) sv[i] = -INFINITY;
         }
 #pragma unroll
-        for (int i = 0; i < CH; ++i) pm[i & 7] = fmaxf(pm[i & 7], sv[i]);
+        for (int i = 0; i < CH; i += 2) pm[(i >> 1) & 7] = fmax3(pm[(i >> 1) & 7], sv[i], sv[i + 1]);
       }
       const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
                              fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
@@ -346,7 +392,10 @@ __global__ void __launch_bounds__(FmCfg<DH, NQ>::THREADS, 1)
       if (NQ == 2 && j >= 1) mbar_wait(&pv_done[t], par(j - 1));
       if (lane == 0) FM_TS(warp, j, 2);
       const uint32_t prow = tmem + FM_TP + buf(j) * 64 + lane_off;  // bf16 pairs
-      float ps[4] = {0.f, 0.f, 0.f, 0.f};
+      float2 ps[4];  // per pair slot q: (even key, odd key) partial row sums
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ps[q] = make_float2(0.f, 0.f);
+      const float2 sl2x2 = make_float2(sl2, sl2), nm2 = make_float2(-m_ref, -m_ref);
 #pragma unroll
       for (int g = 0; g < FM_BK / CH; ++g) {  // exp2, row sum, bf16 P row
         if (NQ != 1) {
@@ -370,17 +419,18 @@ __global__ void __launch_bounds__(FmCfg<DH, NQ>::THREADS, 1)
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const int i0 = h * 8 + 2 * q;  // masked keys hold -inf: exp2 -> +0
-            const float x0 = fmaf(sv[i0], sl2, -m_ref), x1 = fmaf(sv[i0 + 1], sl2, -m_ref);
-            const float p0 = q < POLY ? poly_exp2(x0) : fast_exp2(x0);
-            const float p1 = q < POLY ? poly_exp2(x1) : fast_exp2(x1);
-            ps[q] += p0 + p1;
-            pk[i0 / 2] = __uint_as_float(pack_bf16(p0, p1));
+            const float2 x = ffma2(make_float2(sv[i0], sv[i0 + 1]), sl2x2, nm2);
+            const float2 pp = q < POLY ? poly_exp2x2(x)
+                                       : make_float2(fast_exp2(x.x), fast_exp2(x.y));
+            ps[q] = fadd2(ps[q], pp);
+            pk[i0 / 2] = __uint_as_float(pack_bf16(pp.x, pp.y));
           }
         }
 #pragma unroll
         for (int c = 0; c < CH / 64; ++c) tmem_st32(prow + g * (CH / 2) + c * 32, pk + c * 32);
       }
-      const float rs = (ps[0] + ps[1]) + (ps[2] + ps[3]);
+      const float rs = ((ps[0].x + ps[0].y) + (ps[1].x + ps[1].y)) +
+                       ((ps[2].x + ps[2].y) + (ps[3].x + ps[3].y));
       l += rs;
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

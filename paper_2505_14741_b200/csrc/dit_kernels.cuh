@@ -270,11 +270,24 @@ __device__ __forceinline__ void store_act4(const LnModArgs& p, int64_t idx, floa
 }
 
 static __global__ void __launch_bounds__(256) ln_mod_kernel(const __grid_constant__ LnModArgs p) {
-  pdl_wait_and_release();
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (row >= p.rows) return;
   const int D4 = p.D >> 2;
+  if (row < p.rows) {
+    // the adaLN rows come from kernels that completed before the predecessor
+    // (PDL chain): pull this lane's shift / scale into L1 while the
+    // predecessor finishes
+    const int b = row / p.L;
+    const int64_t mrow = p.use_rows ? p.mod_row[b] : b;
+    const int td = (p.txt && row % p.L < p.txt) ? p.txt_delta : 0;
+    const float* base = p.mod + mrow * p.mod_stride + td;
+    for (int i = lane; i < D4; i += 32) {
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(base + p.shift_off + 4 * i));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(base + p.scale_off + 4 * i));
+    }
+  }
+  pdl_wait_and_release();
+  if (row >= p.rows) return;
   const float4* hr = reinterpret_cast<const float4*>(p.h + (int64_t)row * p.D);
   float4 v[LN_MAXV];
   float s = 0.f;

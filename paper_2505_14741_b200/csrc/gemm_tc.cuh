@@ -439,23 +439,42 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) TC_STAMP(1);
   // the prologue above overlaps the predecessor's tail (PDL); operands and
-  // epilogue inputs are only touched after it completes
+  // epilogue inputs are only touched after it completes - except the weight
+  // tiles (B), which no kernel writes: the producer issues the first ring's
+  // worth of B loads before its PDL wait, so their (HBM) latency overlaps the
+  // predecessor's tail, then A once the predecessor is done
+  const bool producer = warp == 0 && lane == 0;
+  const int npre = (producer && !(dbg & 2)) ? (nk < TC_STAGES ? nk : TC_STAGES) : 0;
+  for (int kb = 0; kb < npre; ++kb) {  // fresh ring: no empty waits
+    uint8_t* st = smem + kb * C::STAGE_BYTES;
+    mbar_expect_tx(&full[kb], C::STAGE_BYTES);
+    const int kx = (kb0 + kb) * C::BK;
+    tma_load_2d(st + C::A_BYTES, &mapB, &full[kb], kx, n0);
+    if (KIND == KIND_TF32X3)
+      tma_load_2d(st + 2 * C::A_BYTES + C::B_BYTES, &mapBlo, &full[kb], kx, n0);
+  }
   pdl_wait_and_release();
   if (threadIdx.x == 0) TC_STAMP(2);
 
-  if (warp == 0 && lane == 0) {
+  if (producer) {
     // ---------------- TMA producer
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % TC_STAGES;
-      mbar_wait(&empty[s], ((kb / TC_STAGES) & 1) ^ 1);
       uint8_t* st = smem + s * C::STAGE_BYTES;
+      const int kx = (kb0 + kb) * C::BK;
+      if (kb < npre) {  // B already in flight: the A half of the stage
+        tma_load_2d(st, &mapA, &full[s], kx, m0);
+        if (KIND == KIND_TF32X3)
+          tma_load_2d(st + C::A_BYTES + C::B_BYTES, &mapAlo, &full[s], kx, m0);
+        continue;
+      }
+      mbar_wait(&empty[s], ((kb / TC_STAGES) & 1) ^ 1);
       if (dbg & 2) {
         mbar_expect_tx(&full[s], 0);
         continue;
       }
       mbar_expect_tx(&full[s], C::STAGE_BYTES);
       if (kb == 0) TC_STAMP(3);
-      const int kx = (kb0 + kb) * C::BK;
       tma_load_2d(st, &mapA, &full[s], kx, m0);
       tma_load_2d(st + C::A_BYTES, &mapB, &full[s], kx, n0);
       if (KIND == KIND_TF32X3) {

@@ -69,25 +69,46 @@ static __global__ void __launch_bounds__(256) gn_stats_kernel(const __grid_const
   __shared__ bool last;
   pdl_wait_and_release();
   const int g = blockIdx.x, b = blockIdx.y, sl = blockIdx.z;
-  const int ctot = p.c1 + p.c2, cpg = ctot / p.G;
-  const int64_t n = (int64_t)p.hw * cpg;
-  const int64_t i0 = n * sl / p.S, i1 = n * (sl + 1) / p.S;
-  auto val = [&](int64_t idx) -> float {
-    const int64_t px = idx / cpg;
-    const int c = g * cpg + (int)(idx % cpg);
-    const int64_t row = (int64_t)b * p.hw + px;
-    return c < p.c1 ? p.in1[row * p.c1 + c] : p.in2[row * p.c2 + (c - p.c1)];
+  const int ctot = p.c1 + p.c2, cpg = ctot / p.G, cg0 = g * cpg;
+  // slice = a contiguous pixel range; a thread walks pixels, reading the
+  // group's cpg channels of each (contiguous: 16-byte loads when aligned and
+  // inside one input of the concatenation); 32-bit index arithmetic
+  const int px0 = (int)((int64_t)p.hw * sl / p.S), px1 = (int)((int64_t)p.hw * (sl + 1) / p.S);
+  const bool one = cg0 + cpg <= p.c1 || cg0 >= p.c1;  // the group lies in in1 or in2
+  const float* src = cg0 < p.c1 ? p.in1 : p.in2;
+  const int cs = cg0 < p.c1 ? p.c1 : p.c2, co = cg0 < p.c1 ? cg0 : cg0 - p.c1;
+  const bool vec = one && (cpg & 3) == 0 && (co & 3) == 0 && (cs & 3) == 0;
+  const int rowb = b * p.hw;
+  auto chan = [&](int row, int c) -> float {  // concatenated channel c of a row
+    return c < p.c1 ? p.in1[(int64_t)row * p.c1 + c] : p.in2[(int64_t)row * p.c2 + (c - p.c1)];
   };
-  float s = 0.f;
-  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) s += val(i);
-  const float cnt = (float)(i1 - i0);
-  const float mean = block_sum(s, red) / cnt;
-  float q = 0.f;
-  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-    const float d = val(i) - mean;
-    q = fmaf(d, d, q);
-  }
-  const float m2 = block_sum(q, red);
+  auto pass = [&](float mean, bool sq) -> float {
+    float acc = 0.f;
+    for (int px = px0 + threadIdx.x; px < px1; px += blockDim.x) {
+      const int row = rowb + px;
+      if (vec) {
+        const float4* q4 = reinterpret_cast<const float4*>(src + (int64_t)row * cs + co);
+        for (int k = 0; k < (cpg >> 2); ++k) {
+          const float4 v = q4[k];
+          if (sq) {
+            const float a = v.x - mean, c = v.y - mean, d = v.z - mean, e = v.w - mean;
+            acc = fmaf(a, a, fmaf(c, c, fmaf(d, d, fmaf(e, e, acc))));
+          } else {
+            acc += (v.x + v.y) + (v.z + v.w);
+          }
+        }
+      } else {
+        for (int k = 0; k < cpg; ++k) {
+          const float v = chan(row, cg0 + k);
+          acc = sq ? fmaf(v - mean, v - mean, acc) : acc + v;
+        }
+      }
+    }
+    return acc;
+  };
+  const float cnt = (float)((px1 - px0) * cpg);
+  const float mean = block_sum(pass(0.f, false), red) / cnt;
+  const float m2 = block_sum(pass(mean, true), red);
   const int bg = b * p.G + g;
   if (threadIdx.x == 0) {
     float* pp = p.partial + ((int64_t)bg * p.S + sl) * 3;

@@ -151,15 +151,15 @@ struct GatherArgs {
 
 static __global__ void __launch_bounds__(256) gather_kernel(const __grid_constant__ GatherArgs p) {
   pdl_wait_and_release();
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // 32-bit index arithmetic (the host keeps total < 2^31): 64-bit divisions
+  // cost ~10x more per thread
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= p.total) return;
   const int ctot = p.c1 + p.c2, chunks = ctot >> 3;
-  const int chunk = (int)(idx % chunks);
-  const int64_t mt = idx / chunks;
-  const int tap = (int)(mt % p.taps);
-  const int64_t m = mt / p.taps;
+  const int mt = idx / chunks, chunk = idx - mt * chunks;
+  const int m = mt / p.taps, tap = mt - m * p.taps;
   const int hwo = p.Ho * p.Wo;
-  const int b = (int)(m / hwo), pix = (int)(m % hwo);
+  const int b = m / hwo, pix = m - b * hwo;
   const int oy = pix / p.Wo, ox = pix % p.Wo;
   int iy = oy, ix = ox;
   bool ok = true;
@@ -215,7 +215,7 @@ static __global__ void __launch_bounds__(256) gather_kernel(const __grid_constan
   u.y = pack_bf16x2(v[2], v[3]);
   u.z = pack_bf16x2(v[4], v[5]);
   u.w = pack_bf16x2(v[6], v[7]);
-  *reinterpret_cast<uint4*>(p.A + m * (int64_t)(p.taps * ctot) + tap * ctot + c0) = u;
+  *reinterpret_cast<uint4*>(p.A + (int64_t)m * (p.taps * ctot) + tap * ctot + c0) = u;
 }
 
 }  // namespace ps
@@ -451,6 +451,7 @@ int ps_unet_forward(ps_unet* h, const float* x, const int32_t* host_ts, int B, f
       g.stats = h->stats;
       g.A = h->scratch;
       g.total = (int64_t)rows * op.taps * ((op.c1 + op.c2) / 8);
+      PS_CHECK_ARG(g.total < (1ll << 31), "gather: operand too large for 32-bit indexing");
       launch_pdl(gather_kernel, dim3((unsigned)((g.total + 255) / 256)), dim3(256), 0, st, g);
       if ((rc = check_launch("gather"))) return rc;
       ++launches;

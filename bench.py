@@ -188,9 +188,10 @@ def cpu_predictor(cfg):
     return DiT(SPECS[cfg["spec"]], seed=0)
 
 
-def cpu_reference_run(cfg, max_forwards=None):
-    """Run the reference's sequential sampler on host cores (oracle predictor
-    injected through its import seam, engines.py:40). Returns
+def cpu_reference_run(cfg, max_forwards=None, degree=1):
+    """Run the reference's sampler on host cores (oracle predictor injected
+    through its import seam, engines.py:40): sequential, or its ParaStep
+    (Algorithm 1 emulation, engines.py:232-277) at degree > 1. Returns
     (elapsed_s, forwards_done, x0 or None, kind)."""
     import numpy as np
 
@@ -214,7 +215,11 @@ def cpu_reference_run(cfg, max_forwards=None):
         RE.forward_batch = lambda w, xs, ts, T: [fwd(w, x, t, T) for x, t in zip(xs, ts)]
         RW.forward = fwd
         sched = RS.make_default_schedule(cfg["T"], cfg["sigma"])
-        rcfg = RE.RunConfig(steps=cfg["T"], seed=0, data_dim=n)
+        if degree > 1:
+            rcfg = RE.RunConfig(steps=cfg["T"], warmup=cfg["warmup"], strategy="parastep",
+                                degree=degree, seed=0, data_dim=n)
+        else:
+            rcfg = RE.RunConfig(steps=cfg["T"], seed=0, data_dim=n)
         t0 = time.perf_counter()
         try:
             x0 = RE.run_strategy(Shim(), sched, rcfg).x0
@@ -777,6 +782,19 @@ def our_arm(args, cfg, world, rank, local):
                                                                             cfg["warmup"], d)
         if not args.no_cpu_baseline:
             cpu, rel = cpu_leg(args, cfg, w, sched, n, torch)
+    if rel is None and world > 1 and args.config in CPU_FULL and not args.no_cpu_baseline:
+        # degree-d parity: the reference's own ParaStep (Algorithm 1) on rank 0's
+        # host cores vs this run's x0 (seed 0, identical on every rank)
+        sampler.run(0, graph=True)
+        torch.cuda.synchronize()
+        if rank == 0 and reference_module()[0] == "reference":
+            from paper_2505_14741_b200.numerics import rel_mae
+
+            _, _, x0_ref, _ = cpu_reference_run(cfg, degree=world)
+            rel = rel_mae(x0_ref, sampler.ops.x.double().cpu().numpy())
+            extra["rel_mae_source"] = (f"x0 (seed 0) vs the reference's ParaStep emulation at "
+                                       f"degree {world} on host cores (run live)")
+        dist.barrier()
     if rel is None:
         rel = fixture_rel(args, cfg, w, sampler, world, rank, torch, extra)
     if world > 1:

@@ -167,7 +167,9 @@ int ps_dit_bench_gemm(ps_dit* h, int which, int B, int iters, void* cuda_stream)
 /* Diagnostic (allocates + synchronises; never on the hot path):
  * C[M,N] = A[M,K] W[K,N] + bias with fp32 buffers in the reference layout,
  * through the tcgen05 kernel (impl 2; precision 1 = bf16, 0 = 3xTF32) or the
- * SIMT fp32 kernel (impl 1). */
+ * SIMT fp32 kernel (impl 1). Test hooks: 3 = split-K segments in one CTA,
+ * 4 = at most 2 cluster CTAs along K, 5 / 6 = bf16 2-SM kernel forced on /
+ * off (5: one pair tile per CTA pair), 7 = the persistent 2-SM kernel. */
 int ps_gemm_test(const float* A, const float* W, const float* bias, float* C, int M, int N, int K,
                  int precision, int impl, void* cuda_stream);
 
@@ -270,8 +272,10 @@ int ps_traj_diff(const void* a, const void* b, const int32_t* rows_a, const int3
 
 /* Diagnostic (allocates + synchronises): softmax(Q K^T / sqrt(dh)) V over
  * qkv fp32 [B*L, 3D] (row m = [q | k | v], heads of dh = D/H contiguous)
- * into out fp32 [B*L, D], operands rounded to bf16: impl 1 = mma.sync flash
- * attention, impl 2 = tcgen05/TMEM flash attention (dh = 64). */
+ * into out fp32 [B*L, D]. bf16 operands (rounded): impl 1 = mma.sync flash
+ * attention, 2 = tcgen05/TMEM flash attention (auto query tiles), 3 / 4 = it
+ * with 1 / 2 query tiles per CTA. fp32 operands: impl 5 = mma.sync 3xTF32,
+ * 6 = tcgen05 3xTF32 (the fp32 predictor path, head_dim <= 64). */
 int ps_attn_test(const float* qkv, float* out, int B, int L, int H, int D, int impl,
                  void* cuda_stream);
 /* Diagnostic: mean device time (us) of `iters` back-to-back attention launches. */

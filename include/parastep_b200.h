@@ -210,6 +210,7 @@ typedef struct ps_unet_op {
   int32_t act;         /* 1 = GELU-tanh epilogue */
   int32_t heads;       /* attention heads (head_dim 64) */
   float eps;           /* GN / LN epsilon */
+  int32_t out2;        /* bf16 shadow of the fp32 output (a later op's A), -1 none */
 } ps_unet_op;
 
 typedef struct ps_unet_config {

@@ -49,7 +49,8 @@ class ps_dit_weights(C.Structure):
 class ps_unet_op(C.Structure):
     _fields_ = [(n, C.c_int32) for n in (
         "kind", "layer", "pre", "in1", "in2", "c1", "c2", "h", "w", "taps", "resample", "cout",
-        "temb_layer", "temb_off", "resid", "out", "out_bf16", "act", "heads")] + [("eps", C.c_float)]
+        "temb_layer", "temb_off", "resid", "out", "out_bf16", "act", "heads")] + [
+        ("eps", C.c_float), ("out2", C.c_int32)]
 
 
 class ps_unet_config(C.Structure):

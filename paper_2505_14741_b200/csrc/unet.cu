@@ -474,6 +474,7 @@ int ps_unet_forward(ps_unet* h, const float* x, const int32_t* host_ts, int B, f
       e.resid = buf(op.resid);
       if (op.out_bf16) e.out_bf16 = (__nv_bfloat16*)h->bufs[op.out];
       else e.out = buf(op.out);
+      if (op.out2 >= 0) e.out_bf16 = (__nv_bfloat16*)h->bufs[op.out2];  // bf16 shadow
       e.act = op.act;
     }
     if ((rc = tc_gemm(h->tcw, op.layer, s.A, rows, op.cout, s.K, e, 1, st))) return rc;

@@ -61,7 +61,7 @@ class UNetWeights:
             o = ops[k]
             for f in ("kind", "layer", "pre", "in1", "in2", "c1", "c2", "h", "w", "taps",
                       "resample", "cout", "temb_layer", "temb_off", "resid", "out", "out_bf16",
-                      "act", "heads", "eps"):
+                      "act", "heads", "eps", "out2"):
                 setattr(o, f, getattr(op, f))
         self._ops = ops
         self._bufp = _lib.ptr_array([_lib.ptr(b) for b in self.bufs])

@@ -112,6 +112,7 @@ class Op:
     resid: int = -1          # buffer added in the epilogue
     out: int = -1            # output buffer id (BUF_EPS for conv_out)
     out_bf16: int = 0        # output written as bf16 (a later op's A operand)
+    out2: int = -1           # bf16 shadow of an fp32 output (a later op's A operand), -1 none
     act: int = 0             # 1 = GELU-tanh epilogue
     heads: int = 0           # OP_ATTN
     eps: float = 1e-5        # GN / LN epsilon of the producer
@@ -199,6 +200,7 @@ def plan(s: UNetSpec) -> Plan:
         qkv = p.buf(hw * 3 * c, bf16=True)
         ob = p.buf(hw * c, bf16=True)
         hid = p.buf(hw * s.mlp_ratio * c, bf16=True)
+        xb = p.buf(hw * c, bf16=True)  # bf16 shadow of x after the last block: proj_out's A
         for d in range(s.depth):
             nd = f"{name}.t{d}"
             lq = p.layer(f"{nd}.qkv", c, 3 * c)
@@ -215,10 +217,13 @@ def plan(s: UNetSpec) -> Plan:
                             s.mlp_ratio * c, out=hid, out_bf16=1, act=1, eps=1e-6,
                             name=f"{nd}.fc1"))
             p.ops.append(Op(OP_LINEAR, l2, PRE_NONE, hid, -1, s.mlp_ratio * c, 0, h, w, 1,
-                            RS_NONE, c, resid=x, out=x, name=f"{nd}.fc2"))
+                            RS_NONE, c, resid=x, out=x, out2=xb if d == s.depth - 1 else -1,
+                            name=f"{nd}.fc2"))
         o = p.buf(hw * c)
         lo = p.layer(f"{name}.proj_out", c, c)
-        p.ops.append(Op(OP_LINEAR, lo, PRE_CONVERT, x, -1, c, 0, h, w, 1, RS_NONE, c, resid=hbuf,
+        # A = the bf16 shadow the last fc2 epilogue wrote (same RN rounding as a
+        # convert gather, one launch fewer)
+        p.ops.append(Op(OP_LINEAR, lo, PRE_NONE, xb, -1, c, 0, h, w, 1, RS_NONE, c, resid=hbuf,
                         out=o, name=f"{name}.proj_out"))
         return o
 

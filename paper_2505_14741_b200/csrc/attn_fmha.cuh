@@ -249,7 +249,11 @@ __global__ void __launch_bounds__(FmCfg<DH, NQ>::THREADS, 1)
       // ---------------- MMA issuer: the whole warp runs the loop (descriptors
       // in uniform registers), one elected lane issues each tcgen05 op
       constexpr uint32_t idS = make_idesc(KIND_BF16, 128, 128);
-      constexpr uint32_t idPV = make_idesc(KIND_BF16, 128, DH) | (1u << 16);  // B (V) MN-major
+      // the zero-padded head dims beyond dh do no tensor work: S runs
+      // ceil(dh/16) K-steps, P V an N of round_up(dh, 16) (DiT-XL/2's 72 -> 80
+      // of the 128-wide operand); O's columns past that are never stored
+      const int kdh = (p.dh + 15) / 16;
+      const uint32_t idPV = make_idesc(KIND_BF16, 128, 16 * kdh) | (1u << 16);  // B (V) MN-major
       // S_t(j) = Q_t K_j^T into S buffer `sb`
       auto issue_s = [&](int t, int j, int sb) {
         const int s = j % FM_STAGES;
@@ -259,6 +263,7 @@ __global__ void __launch_bounds__(FmCfg<DH, NQ>::THREADS, 1)
         const uint8_t* qt = smem + FM_Q_OFF + t * NA * FM_TILE;
 #pragma unroll
         for (int k = 0; k < DH / 16; ++k) {  // atom k/4, +32 B along K inside it
+          if (k >= kdh) break;
           const uint64_t qd = smem_desc_sw128(qt + (k >> 2) * FM_TILE) + 2 * (k & 3);
           const uint64_t kd = smem_desc_sw128(kt + (k >> 2) * FM_TILE) + 2 * (k & 3);
           umma_e<KIND_BF16>(tmem + 128 * sb, qd, kd, idS, k > 0 ? 1u : 0u);

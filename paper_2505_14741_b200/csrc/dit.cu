@@ -264,8 +264,11 @@ double ps_dit_flops(const ps_dit* h) { return h ? h->flops : 0.0; }
 
 int ps_dit_kernels_per_forward(const ps_dit* h) {
   // (3 conditioning GEMVs unless the run's table is in use) + patch embed +
-  // 7 per block + final LN + final GEMM
-  return h ? (h->cond_rows > 0 ? 0 : 3) + 1 + 7 * h->depth + 2 : 0;
+  // 7 per block + final LN + final GEMM (one fused final-layer kernel when
+  // the lane is short)
+  if (!h) return 0;
+  const bool fused_final = h->use_tc && (h->P == 16 || h->P == 64) && h->L <= 4096;
+  return (h->cond_rows > 0 ? 0 : 3) + 1 + 7 * h->depth + (fused_final ? 1 : 2);
 }
 
 int ps_dit_bench_gemm(ps_dit* h, int which, int B, int iters, void* cs) {
@@ -489,6 +492,38 @@ int ps_dit_forward(ps_dit* h, const float* x, const int32_t* host_ts, int B, flo
     if ((rc = gemm(h, 4 * i + 3, h->hid, hop, bw.fc2, M, D, h->Dm, e, st))) return rc;
   }
   const int fb = h->depth * h->ada_w;
+  // (decided per lane length, so every batch of a handle takes the same path:
+  // batch == single, bitwise)
+  if (h->use_tc && L <= 4096 && (h->P == 16 || h->P == 64) && D / 4 <= 32 * LN_MAXV) {
+    // small row counts: LN + modulate + projection + unpatchify in one
+    // warp-per-row kernel (final_layer_kernel) instead of LN-modulate + GEMM
+    FinalArgs fa{};
+    fa.ln.h = h->h;
+    fa.ln.rows = M;
+    fa.ln.D = D;
+    fa.ln.L = L;
+    fa.ln.mod = modb;
+    fa.ln.mod_stride = h->n_ada;
+    if (h->rows_on) {
+      fa.ln.use_rows = 1;
+      memcpy(fa.ln.mod_row, h->lane_mod_row, sizeof(fa.ln.mod_row));
+    }
+    fa.ln.shift_off = fb;
+    fa.ln.scale_off = fb + D;
+    fa.ln.txt = h->txt;
+    fa.W = h->Wfo;
+    fa.bias = h->bfo;
+    fa.P = h->P;
+    fa.g = h->g;
+    fa.eps = eps_out;
+    fa.n_latent = h->n_latent;
+    const dim3 grid((M * 32 + 255) / 256);
+    if (h->P == 16)
+      launch_pdl(final_layer_kernel<16>, grid, dim3(256), 0, st, fa);
+    else
+      launch_pdl(final_layer_kernel<64>, grid, dim3(256), 0, st, fa);
+    return check_launch("final_layer");
+  }
   if ((rc = ln_mod(h, M, fb, fb + D, aop, st))) return rc;
   Epi e{};
   e.mode = EPI_UNPATCH;

@@ -333,6 +333,118 @@ static __global__ void __launch_bounds__(256) ln_mod_kernel(const __grid_constan
   }
 }
 
+// ---------------------------------------------------------------- final layer
+// The DiT's final layer as ONE warp-per-row kernel for small row counts:
+// LayerNorm (two-pass, registers) + the final adaLN modulate + the linear
+// projection to the P patch features (fp32 FMA, W in the reference layout
+// (D, P)) + bias + the unpatchify scatter into eps. Replaces LN-modulate +
+// a split-K tensor-core GEMM of N = P (16 for the 4-channel latents) - two
+// launches and an A round trip - where the GEMM is tiny. Text rows (m % L <
+// txt) carry no latent output and are skipped.
+constexpr int FL_MAXP = 64;  // P <= 64 (4 and 16 channels x 2x2 patches)
+
+struct FinalArgs {
+  LnModArgs ln;  // h, rows, D, L, mod rows, shift/scale offsets (txt rows skipped)
+  const float* W;  // [D][P] fp32
+  const float* bias;  // [P]
+  int P;
+  DitGeom g;
+  float* eps;
+  int64_t n_latent;
+};
+
+template <int P>
+static __global__ void __launch_bounds__(256) final_layer_kernel(const __grid_constant__ FinalArgs f) {
+  const LnModArgs& p = f.ln;
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int D4 = p.D >> 2;
+  if (row < p.rows) {  // adaLN rows: written >= 2 kernels earlier (see ln_mod_kernel)
+    const int b = row / p.L;
+    const int64_t mrow = p.use_rows ? p.mod_row[b] : b;
+    const float* base = p.mod + mrow * p.mod_stride;
+    for (int i = lane; i < D4; i += 32) {
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(base + p.shift_off + 4 * i));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(base + p.scale_off + 4 * i));
+    }
+  }
+  pdl_wait_and_release();
+  if (row >= p.rows) return;
+  const int b = row / p.L, l = row % p.L - p.txt;
+  if (l < 0) return;  // text row
+  const float4* hr = reinterpret_cast<const float4*>(p.h + (int64_t)row * p.D);
+  float4 v[LN_MAXV];
+  float s = 0.f;
+#pragma unroll
+  for (int u = 0; u < LN_MAXV; ++u) {
+    const int i = lane + 32 * u;
+    v[u] = i < D4 ? hr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    s += (v[u].x + v[u].y) + (v[u].z + v[u].w);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float mu = s / p.D;
+  float q = 0.f;
+#pragma unroll
+  for (int u = 0; u < LN_MAXV; ++u) {
+    if (lane + 32 * u < D4) {
+      const float a = v[u].x - mu, c = v[u].y - mu, d = v[u].z - mu, e = v[u].w - mu;
+      q = fmaf(a, a, fmaf(c, c, fmaf(d, d, fmaf(e, e, q))));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  const float rstd = rsqrtf(q / p.D + 1e-6f);
+  const int64_t mrow = p.use_rows ? p.mod_row[b] : b;
+  const float4* sh = reinterpret_cast<const float4*>(p.mod + mrow * p.mod_stride + p.shift_off);
+  const float4* sc = reinterpret_cast<const float4*>(p.mod + mrow * p.mod_stride + p.scale_off);
+  // this lane's k = 4 (lane + 32 u) + j: partial dot products for all P outputs
+  float acc[P];
+#pragma unroll
+  for (int j = 0; j < P; ++j) acc[j] = 0.f;
+#pragma unroll
+  for (int u = 0; u < LN_MAXV; ++u) {
+    const int i = lane + 32 * u;
+    if (i >= D4) break;
+    const float4 a = sh[i], c = sc[i];
+    const float y[4] = {fmaf((v[u].x - mu) * rstd, 1.f + c.x, a.x),
+                        fmaf((v[u].y - mu) * rstd, 1.f + c.y, a.y),
+                        fmaf((v[u].z - mu) * rstd, 1.f + c.z, a.z),
+                        fmaf((v[u].w - mu) * rstd, 1.f + c.w, a.w)};
+#pragma unroll
+    for (int j4 = 0; j4 < 4; ++j4) {
+      const float4* wr = reinterpret_cast<const float4*>(f.W + (int64_t)(4 * i + j4) * P);
+#pragma unroll
+      for (int c4 = 0; c4 < P / 4; ++c4) {
+        const float4 w = __ldg(wr + c4);
+        acc[4 * c4] = fmaf(y[j4], w.x, acc[4 * c4]);
+        acc[4 * c4 + 1] = fmaf(y[j4], w.y, acc[4 * c4 + 1]);
+        acc[4 * c4 + 2] = fmaf(y[j4], w.z, acc[4 * c4 + 2]);
+        acc[4 * c4 + 3] = fmaf(y[j4], w.w, acc[4 * c4 + 3]);
+      }
+    }
+  }
+  // fixed-order butterfly over the warp, then lane j scatters output j
+#pragma unroll
+  for (int j = 0; j < P; ++j) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+  }
+  float mine = 0.f;
+#pragma unroll
+  for (int j = 0; j < P; ++j)
+    if ((j & 31) == lane) mine = acc[j];
+  for (int j = lane; j < P; j += 32) {
+    float out = j < 32 ? mine : 0.f;
+    if (j >= 32) {  // P > 32: the second half (lane j - 32 already holds acc[j])
+#pragma unroll
+      for (int jj = 32; jj < P; ++jj)
+        if (jj == j) out = acc[jj];
+    }
+    f.eps[(int64_t)b * f.n_latent + patch_elem_index(f.g, l, j)] = out + (f.bias ? f.bias[j] : 0.f);
+  }
+}
+
 // ---------------------------------------------------------------- attention
 // Flash-style SIMT attention, fp32. qkv row m = [q(D) | k(D) | v(D)], head h
 // in columns h*dh..; out row m = heads concatenated (spec.py). One block per
